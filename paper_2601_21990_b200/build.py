@@ -1,0 +1,74 @@
+"""In-tree build of the CUDA C-ABI library (and the test oracles).
+
+nvcc for sm_100a only; fp64 everywhere with --fmad=false so every rounding
+matches the reference C++ (built without FMA contraction). The .so lands in
+paper_2601_21990_b200/lib/ and travels with the repository snapshot.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIBDIR = os.path.join(HERE, "lib")
+LIB = os.path.join(LIBDIR, "libbatchlp_cuda.so")
+SOURCES = ["bl_kernels.cu", "bl_solver.cu", "bl_generators.cpp"]
+HEADERS = ["bl_device.cuh"]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
+    "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
+    "-shared",
+]
+
+
+def _nvcc() -> str:
+    cand = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    return cand
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_library(force: bool = False, verbose: bool = False) -> str:
+    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
+    deps.append(os.path.join(ROOT, "include", "batchlp_cuda.h"))
+    if not force and not _stale(LIB, deps):
+        return LIB
+    os.makedirs(LIBDIR, exist_ok=True)
+    tmp = LIB + ".tmp"
+    cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"),
+           *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True, cwd=CSRC)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+def build_oracles(verbose: bool = False) -> None:
+    """oracle/Makefile: the C restatement always; the reference shim only
+    where /root/reference exists (the GPU box uses the prebuilt .so)."""
+    targets = []
+    if os.path.exists(os.path.join(ROOT, "oracle", "batchlp_oracle.c")):
+        targets.append("oracle")
+    if os.path.isdir("/root/reference/proj/include"):
+        targets.append("ref")
+    cmd = ["make", "-s", "-C", os.path.join(ROOT, "oracle"), *targets]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+
+
+if __name__ == "__main__":
+    build_library(force="--force" in sys.argv, verbose=True)
+    build_oracles(verbose=True)
