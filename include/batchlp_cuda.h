@@ -145,7 +145,19 @@ typedef struct bl_summary {
   uint64_t trajectory_hash;
   double eta;      /* step size used */
   double device_ms;/* device time of the solve (CUDA events), setup included */
+  int64_t kernel_launches; /* kernels the solve launched on the device */
+  int64_t loop_passes;     /* operator applications (iterations + restarts) */
 } bl_summary;
+
+/* In-situ timing of one kernel kind over the last solve: device
+ * %globaltimer span of each launch (first CTA entry to last CTA exit) and
+ * the algorithmic bytes credited to it. */
+typedef struct bl_kernel_stat {
+  char name[16];
+  double launches;
+  double total_ns;
+  double alg_bytes;
+} bl_kernel_stat;
 
 /* ---- context ------------------------------------------------------------ */
 void bl_config_default(bl_config* cfg);
@@ -206,6 +218,8 @@ int bl_fetch_solution(bl_ctx* ctx, int32_t column, double* x, double* y,
                       double* reduced);
 int bl_fetch_certificate(bl_ctx* ctx, int32_t column, double* delta_x,
                          double* delta_y, double* delta_r);
+/* Per-kernel timing of the last solve (up to cap kinds). */
+int bl_fetch_profile(bl_ctx* ctx, bl_kernel_stat* out, int32_t cap, int32_t* n_out);
 /* Copies min(cap, restart_log_size) events; returns the count in *n_out. */
 int bl_fetch_restart_log(bl_ctx* ctx, bl_restart_event* out, int32_t cap,
                          int32_t* n_out);

@@ -168,7 +168,8 @@ def append_cutoff(p, alpha):
 
 def spectral_norm(p) -> float:
     out = C.c_double()
-    _chk(lib().ref_spectral_norm(RefLp.from_problem(p).h, C.byref(out)))
+    h = RefLp.from_problem(p)
+    _chk(lib().ref_spectral_norm(h.h, C.byref(out)))
     return out.value
 
 

@@ -95,6 +95,17 @@ class bl_summary(C.Structure):
         ("trajectory_hash", C.c_uint64),
         ("eta", C.c_double),
         ("device_ms", C.c_double),
+        ("kernel_launches", C.c_int64),
+        ("loop_passes", C.c_int64),
+    ]
+
+
+class bl_kernel_stat(C.Structure):
+    _fields_ = [
+        ("name", C.c_char * 16),
+        ("launches", C.c_double),
+        ("total_ns", C.c_double),
+        ("alg_bytes", C.c_double),
     ]
 
 
@@ -144,6 +155,8 @@ SIGNATURES = {
     ),
     "bl_fetch_solution": (C.c_int, [_P, C.c_int32, _DP, _DP, _DP]),
     "bl_fetch_certificate": (C.c_int, [_P, C.c_int32, _DP, _DP, _DP]),
+    "bl_fetch_profile": (
+        C.c_int, [_P, C.POINTER(bl_kernel_stat), C.c_int32, _IP]),
     "bl_fetch_restart_log": (
         C.c_int, [_P, C.POINTER(bl_restart_event), C.c_int32, _IP]),
     "bl_gen_set_cover": (

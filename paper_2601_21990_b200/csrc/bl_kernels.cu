@@ -216,7 +216,7 @@ __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
     const int r0 = min(rows, r * per), r1 = min(rows, r0 + per);
     const int cnt = r1 - r0;
     int gs, ge;
-    if (cnt <= kTinyRows) {
+    if (rows <= kTinyRows) {  // whole dimension tiny: one sequential walk
       gs = g == 0 ? r0 : r1;
       ge = r1;
     } else {
@@ -351,9 +351,11 @@ template <int W, bool CHECK>
 __global__ void __launch_bounds__(kBlock) k_primal(Params P) {
   const Ctrl C = *P.ctrl;
   if (C.done) return;
+  prof_begin(P, K_PRIMAL);
   PrimalOp<W, CHECK> op(P, C);
   const int nb = (C.active + W - 1) / W;
   run_rows<W, 2>(op, P.n, nb, C.Rp, P.partials, P.counters, P.colsum, S_DX2, P.Kp);
+  prof_end(P, K_PRIMAL);
 }
 
 // ---------------------------------------------------------------------------
@@ -452,10 +454,12 @@ template <int W, bool CHECK>
 __global__ void __launch_bounds__(kBlock) k_dual(Params P) {
   const Ctrl C = *P.ctrl;
   if (C.done) return;
+  prof_begin(P, K_DUAL);
   DualOp<W, CHECK> op(P, C);
   const int nb = (C.active + W - 1) / W;
   run_rows<W, DualOp<W, CHECK>::NS>(op, P.m, nb, C.Rd, P.partials, P.counters,
                                     P.colsum, S_DY2, P.Kp);
+  prof_end(P, K_DUAL);
 }
 
 // ---------------------------------------------------------------------------
@@ -537,9 +541,11 @@ template <int W>
 __global__ void __launch_bounds__(kBlock) k_check(Params P) {
   const Ctrl C = *P.ctrl;
   if (C.done || !C.check) return;
+  prof_begin(P, K_CHECK);
   CheckOp<W> op(P, C);
   const int nb = (C.active + W - 1) / W;
   run_rows<W, 10>(op, P.n, nb, C.Rc, P.partials, P.counters, P.colsum, S_OBJ, P.Kp);
+  prof_end(P, K_CHECK);
 }
 
 // ---------------------------------------------------------------------------
@@ -579,9 +585,11 @@ template <int W>
 __global__ void __launch_bounds__(kBlock) k_cert(Params P) {
   const Ctrl C = *P.ctrl;
   if (C.done || !C.cert_pending) return;
+  prof_begin(P, K_CERT);
   CertOp<W> op(P, C);
   const int nb = (C.active + W - 1) / W;
   run_rows<W, 1>(op, P.n, nb, C.Rc, P.partials, P.counters, P.colsum, S_CERT, P.Kp);
+  prof_end(P, K_CERT);
 }
 
 // ---------------------------------------------------------------------------
@@ -1066,6 +1074,30 @@ __device__ void finalize(const Params& P, Ctrl& C, double mean, double* sh,
   }
 }
 
+// Folds the finished launches' entry/exit stamps into the accumulators and
+// credits this iteration's row kernels with their algorithmic bytes
+// (compulsory traffic, gathers counted once).
+__device__ void prof_fold(const Params& P, const Ctrl& C) {
+  if (!P.prof) return;
+  const unsigned long long now = gtime();
+  for (int k = 0; k < K_KINDS; ++k) {
+    const unsigned long long s = P.prof[2 * k], e = P.prof[2 * k + 1];
+    if (e != 0ull && s != ~0ull && e >= s) {
+      P.prof_acc[3 * k] += (double)(e - s);
+      P.prof_acc[3 * k + 1] += 1.0;
+    }
+    P.prof[2 * k] = ~0ull;
+    P.prof[2 * k + 1] = 0ull;
+  }
+  P.prof[2 * K_DECIDE] = now;
+  const double n = P.n, m = P.m, nnz = (double)P.nnz, K = C.active;
+  const double chk = C.check ? 1.0 : 0.0;
+  P.prof_acc[3 * K_PRIMAL + 2] += 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 4.0 * n + chk * n);
+  P.prof_acc[3 * K_DUAL + 2] += 12.0 * nnz + 4.0 * (m + 1) + 16.0 * m + 8.0 * K * (n + 6.0 * m + chk * 3.0 * m);
+  if (C.check)
+    P.prof_acc[3 * K_CHECK + 2] += 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 5.0 * n);
+}
+
 __global__ void __launch_bounds__(kDecideThreads) k_decide(Params P, int phase) {
   double* scratch = P.scratch;
   __shared__ double sh[kDecideThreads];
@@ -1079,7 +1111,15 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(Params P, int phase) 
   const int active = C.active;
   double mean;
   if (phase == 0) {
-    if (tid == 0) ish[3] = 0;
+    if (tid == 0) {
+      ish[3] = 0;
+      prof_fold(P, C);
+      C.launches += 3 + (C.check ? 1 : 0);
+      C.passes += 1;
+      // a loop pass either advances total_k or is the single re-application
+      // after a restart, so this bound is never reached by a correct run
+      if (C.passes > 2 * P.max_it + 1024) ish[3] = 2;
+    }
     __syncthreads();
     for (int j = tid; j < active; j += kDecideThreads) {
       int err = 0;
@@ -1090,7 +1130,8 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(Params P, int phase) 
     __syncthreads();
     if (ish[3]) {
       if (tid == 0) {
-        C.error = BL_ERR_DOMAIN;
+        C.error = ish[3] == 2 ? BL_ERR_LOGIC : BL_ERR_DOMAIN;
+        if (P.prof) atomicMax(&P.prof[2 * K_DECIDE + 1], gtime());
         C.done = 1;
         *P.ctrl = C;
         set_cond(P, P.h_loop, 0u);
@@ -1127,8 +1168,10 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(Params P, int phase) 
         if (tid == 0) {
           C.sparse_products += ish[0];
           C.cert_pending = 1;
+          C.launches += 2;
           *P.ctrl = C;
           set_cond(P, P.h_cert, 1u);
+          if (P.prof) atomicMax(&P.prof[2 * K_DECIDE + 1], gtime());
         }
         return;
       }
@@ -1146,7 +1189,12 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(Params P, int phase) 
   }
   finalize(P, C, mean, sh, ish, scratch);
   __syncthreads();
-  if (tid == 0) *P.ctrl = C;
+  if (tid == 0) {
+    if (C.n_snap > 0 || C.n_moves > 0) C.launches += 2;
+    if (C.hash_pending) C.launches += 1;
+    *P.ctrl = C;
+    if (P.prof) atomicMax(&P.prof[2 * K_DECIDE + 1], gtime());
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1156,6 +1204,7 @@ __global__ void k_snapshot(Params P) {
   const Ctrl C = *P.ctrl;
   const int ns = C.n_snap;
   if (ns == 0) return;
+  prof_begin(P, K_SNAPSHOT);
   const int n = P.n, m = P.m, W = P.W;
   const double* Xold = P.X[C.snap_cur];
   const long long total = (long long)ns * (n + m);
@@ -1193,6 +1242,7 @@ __global__ void k_snapshot(Params P) {
       if (bits & SN_CAP) P.RY[ro] = P.BY[e];
     }
   }
+  prof_end(P, K_SNAPSHOT);
 }
 
 // Column moves of the swap-with-last compaction (batch_solver.hpp:143-156,
@@ -1207,6 +1257,7 @@ __global__ void k_compact(Params P) {
   const Ctrl C = *P.ctrl;
   const int nm = C.n_moves;
   if (nm == 0) return;
+  prof_begin(P, K_COMPACT);
   const int n = P.n, m = P.m, W = P.W;
   const bool halpern = !C.anchor_reset;
   const double a = C.alpha_used, oma = 1.0 - a;
@@ -1247,6 +1298,7 @@ __global__ void k_compact(Params P) {
       if (best) P.BY[d] = P.BY[s];
     }
   }
+  prof_end(P, K_COMPACT);
 }
 
 // FNV-1a over the bytes of X[:,0] then Y[:,0] (solver.hpp:170-177,

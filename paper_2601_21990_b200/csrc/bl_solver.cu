@@ -91,7 +91,7 @@ struct bl_ctx {
     B_X0, B_X1, B_Y0, B_Y1, B_AX0, B_AX1, B_aX, B_aY, B_aAX, B_XT, B_YT, B_DY,
     B_RC, B_R, B_DR, B_AXT, B_BX, B_BY, B_BR, B_RX, B_RY, B_RR, B_RDX, B_RDY, B_RDR,
     B_SLOTD, B_SLOTI, B_ORIGI, B_RES, B_COLSUM, B_PART, B_CNT, B_SNAP, B_MOVES,
-    B_LOG, B_CTRL, B_OV, B_OVD, B_WARMX, B_WARMY, B_PI, B_TMP0, B_TMP1, B_COUNT
+    B_LOG, B_CTRL, B_PROF, B_PROFACC, B_OV, B_OVD, B_WARMX, B_WARMY, B_PI, B_TMP0, B_TMP1, B_COUNT
   };
   DevBuf buf[B_COUNT];
   // last solve
@@ -99,6 +99,7 @@ struct bl_ctx {
   int last_width = 0, last_n = 0, last_m = 0, last_vectors = 0;
   std::vector<bl_column_result> last_res;
   int last_log = 0;
+  std::vector<bl_kernel_stat> last_prof;
   // graph cache
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
@@ -556,6 +557,20 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.log = static_cast<bl_restart_event*>(
       ctx->buf[bl_ctx::B_LOG].ensure(sizeof(bl_restart_event) * (size_t)P.log_cap));
   P.ctrl = static_cast<bl::Ctrl*>(ctx->buf[bl_ctx::B_CTRL].ensure(sizeof(bl::Ctrl)));
+  P.prof = static_cast<unsigned long long*>(
+      ctx->buf[bl_ctx::B_PROF].ensure(sizeof(unsigned long long) * 2 * bl::K_KINDS));
+  P.prof_acc = static_cast<double*>(
+      ctx->buf[bl_ctx::B_PROFACC].ensure(sizeof(double) * 3 * bl::K_KINDS));
+  P.nnz = p->nnz;
+  {
+    unsigned long long hp[2 * bl::K_KINDS];
+    for (int k = 0; k < bl::K_KINDS; ++k) {
+      hp[2 * k] = ~0ull;
+      hp[2 * k + 1] = 0ull;
+    }
+    ck(cudaMemcpyAsync(P.prof, hp, sizeof(hp), cudaMemcpyHostToDevice, s), "prof");
+    ck(cudaMemsetAsync(P.prof_acc, 0, sizeof(double) * 3 * bl::K_KINDS, s), "prof acc");
+  }
   {
     const size_t nov = std::max<size_t>(ovs.size(), 1);
     int* ovi = static_cast<int*>(ctx->buf[bl_ctx::B_OV].ensure(sizeof(int) * 2 * nov));
@@ -652,12 +667,18 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
      "results");
   std::vector<int> done(width);
   ck(cudaMemcpyAsync(done.data(), P.orig_done, sizeof(int) * width, cudaMemcpyDeviceToHost, s), "done");
+  unsigned long long hprof[2 * bl::K_KINDS];
+  double hacc[3 * bl::K_KINDS];
+  ck(cudaMemcpyAsync(hprof, P.prof, sizeof(hprof), cudaMemcpyDeviceToHost, s), "prof");
+  ck(cudaMemcpyAsync(hacc, P.prof_acc, sizeof(hacc), cudaMemcpyDeviceToHost, s), "prof acc");
   ck(cudaEventRecord(ctx->ev1, s), "event");
   ck(cudaStreamSynchronize(s), "solve sync");
   const bl::Ctrl C = *ctx->h_ctrl;
   if (C.error == BL_ERR_DOMAIN)
     raise(BL_ERR_DOMAIN,
           "residual metric is not positive semidefinite; step size exceeds 1/||A||");
+  if (C.error == BL_ERR_LOGIC)
+    raise(BL_ERR_LOGIC, "solve_batch: loop pass bound exceeded (internal error)");
   for (int j = 0; j < width; ++j)
     if (!done[j]) raise(BL_ERR_LOGIC, "solve_batch: column finished without a result");
   float ms = 0.f;
@@ -669,6 +690,25 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   sum.trajectory_hash = C.hash;
   sum.eta = eta;
   sum.device_ms = ms;
+  sum.kernel_launches = C.launches + 2;  // + init and AX = A X
+  sum.loop_passes = C.passes;
+  {
+    static const char* names[bl::K_KINDS] = {"primal", "dual", "check", "decide",
+                                             "cert", "snapshot", "compact", "trace"};
+    ctx->last_prof.assign(bl::K_KINDS, bl_kernel_stat{});
+    for (int k = 0; k < bl::K_KINDS; ++k) {
+      bl_kernel_stat& st = ctx->last_prof[k];
+      std::snprintf(st.name, sizeof(st.name), "%s", names[k]);
+      st.total_ns = hacc[3 * k];
+      st.launches = hacc[3 * k + 1];
+      st.alg_bytes = hacc[3 * k + 2];
+      const unsigned long long b = hprof[2 * k], e = hprof[2 * k + 1];
+      if (e != 0ull && b != ~0ull && e >= b) {  // launches after the last fold
+        st.total_ns += (double)(e - b);
+        st.launches += 1.0;
+      }
+    }
+  }
   if (summary) *summary = sum;
   ctx->last_res = dres;
   for (int j = 0; j < width; ++j)
@@ -905,6 +945,14 @@ int bl_fetch_certificate(bl_ctx* ctx, int32_t column, double* dx, double* dy,
                                  sizeof(double) * n, cudaMemcpyDeviceToHost, s), "fetch dr");
     }
     ck(cudaStreamSynchronize(s), "fetch sync");
+  });
+}
+
+int bl_fetch_profile(bl_ctx* ctx, bl_kernel_stat* out, int32_t cap, int32_t* n_out) {
+  return guarded(ctx, [&] {
+    const int k = std::min<int>(cap, (int)ctx->last_prof.size());
+    for (int i = 0; i < k; ++i) out[i] = ctx->last_prof[i];
+    if (n_out) *n_out = k;
   });
 }
 

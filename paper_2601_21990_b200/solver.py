@@ -168,6 +168,9 @@ class BatchSolveSummary:
     # extension
     eta: float = 0.0
     device_ms: float = 0.0
+    kernel_launches: int = 0
+    loop_passes: int = 0
+    profile: Dict[str, tuple] = field(default_factory=dict)  # kind -> (launches, ns, bytes)
 
 
 # ---------------------------------------------------------------------------
@@ -342,8 +345,15 @@ def solve_batch(batch: BatchProblem, cfg: Optional[SolverConfig] = None,
     out.trajectory_hash = int(summ.trajectory_hash)
     out.eta = summ.eta
     out.device_ms = summ.device_ms
+    out.kernel_launches = int(summ.kernel_launches)
+    out.loop_passes = int(summ.loop_passes)
     if width == 0:
         return out
+    stats = (N.bl_kernel_stat * 16)()
+    got = C.c_int32()
+    _check(ws.ctx.handle, L.bl_fetch_profile(ws.ctx.handle, stats, 16, C.byref(got)))
+    out.profile = {st.name.decode(): (st.launches, st.total_ns, st.alg_bytes)
+                   for st in stats[:got.value]}
     if summ.restart_log_size > 0:
         ev = (N.bl_restart_event * summ.restart_log_size)()
         got = C.c_int32()
