@@ -39,6 +39,9 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+
 #include "bl_device.cuh"
 
 namespace bl {
@@ -149,14 +152,15 @@ __device__ __forceinline__ void gather_row(const int* __restrict__ rp,
 // acc[s][v]: this lane's sums for slots (b*W + li*V + v). Reduces over the
 // CTA in a fixed tree, writes the item's partials, and the last CTA of block
 // b folds all R partials in item order into colsum[s0+s][slot].
+// `red` is a shared buffer of at least kRedDoubles doubles.
 template <int W, int NS>
 __device__ __forceinline__ void publish_item(double (&acc)[NS][Geo<W>::V], int b,
                                              int r, int R, double* partials,
                                              int* counters, double* colsum,
-                                             int s0, int Kp) {
+                                             int s0, int Kp, double* red) {
   using Gm = Geo<W>;
   constexpr int V = Gm::V, L = Gm::L;
-  __shared__ double red[kWarps][NS][W];
+  static_assert(kWarps * NS * W <= kRedDoubles, "reduction buffer too small");
   __shared__ int last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #pragma unroll
@@ -171,14 +175,14 @@ __device__ __forceinline__ void publish_item(double (&acc)[NS][Geo<W>::V], int b
 #pragma unroll
     for (int s = 0; s < NS; ++s)
 #pragma unroll
-      for (int v = 0; v < V; ++v) red[warp][s][lane * V + v] = acc[s][v];
+      for (int v = 0; v < V; ++v) red[(warp * NS + s) * W + lane * V + v] = acc[s][v];
   }
   __syncthreads();
   for (int t = tid; t < NS * W; t += kBlock) {
     const int s = t / W, jj = t - s * W;
     double sum = 0.0;
 #pragma unroll
-    for (int wp = 0; wp < kWarps; ++wp) sum = __dadd_rn(sum, red[wp][s][jj]);
+    for (int wp = 0; wp < kWarps; ++wp) sum = __dadd_rn(sum, red[(wp * NS + s) * W + jj]);
     partials[((size_t)(b * R + r) * NS + s) * W + jj] = sum;
   }
   __threadfence();
@@ -187,12 +191,40 @@ __device__ __forceinline__ void publish_item(double (&acc)[NS][Geo<W>::V], int b
   __syncthreads();
   if (last) {
     __threadfence();
-    for (int t = tid; t < NS * W; t += kBlock) {
-      const int s = t / W, jj = t - s * W;
+    constexpr int Q = NS * W;  // outputs of this block
+    if constexpr (Q <= kBlock) {
+      // T threads per output; thread `part` folds items part, part+T, ...
+      // in order, then the T partial folds are added in part order. Fixed
+      // order for any timing; with R = 1 it is the single partial exactly.
+      double* fold = red;  // free again: the item partials are written
+      constexpr int T = kBlock / Q;
+      const int q = tid % Q, part = tid / Q;
       double sum = 0.0;
-      for (int rr = 0; rr < R; ++rr)
-        sum = __dadd_rn(sum, __ldcg(&partials[((size_t)(b * R + rr) * NS + s) * W + jj]));
-      colsum[(size_t)(s0 + s) * Kp + b * W + jj] = sum;
+      if (part < T) {
+        const int s = q / W, jj = q - s * W;
+        const double* src = partials + ((size_t)b * R * NS + s) * W + jj;
+#pragma unroll 8
+        for (int rr = part; rr < R; rr += T)
+          sum = __dadd_rn(sum, __ldcg(src + (size_t)rr * NS * W));
+      }
+      fold[tid] = sum;
+      __syncthreads();
+      if (tid < Q) {
+        double tot = 0.0;
+#pragma unroll
+        for (int pp = 0; pp < T; ++pp) tot = __dadd_rn(tot, fold[pp * Q + tid]);
+        const int s = tid / W, jj = tid - s * W;
+        colsum[(size_t)(s0 + s) * Kp + b * W + jj] = tot;
+      }
+    } else {
+      for (int t = tid; t < Q; t += kBlock) {
+        const int s = t / W, jj = t - s * W;
+        const double* src = partials + ((size_t)b * R * NS + s) * W + jj;
+        double sum = 0.0;
+#pragma unroll 8
+        for (int rr = 0; rr < R; ++rr) sum = __dadd_rn(sum, __ldcg(src + (size_t)rr * NS * W));
+        colsum[(size_t)(s0 + s) * Kp + b * W + jj] = sum;
+      }
     }
     if (tid == 0) counters[b] = 0;
   }
@@ -205,7 +237,7 @@ __device__ __forceinline__ void publish_item(double (&acc)[NS][Geo<W>::V], int b
 template <int W, int NS, class Op>
 __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
                                          double* partials, int* counters,
-                                         double* colsum, int s0, int Kp) {
+                                         double* colsum, int s0, int Kp, double* red) {
   using Gm = Geo<W>;
   constexpr int V = Gm::V, L = Gm::L, G = Gm::G;
   const int tid = threadIdx.x, g = tid / L, li = tid - g * L;
@@ -232,7 +264,7 @@ __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
     const int slot0 = b * W + li * V;
     op.begin(b, slot0, acc, r == 0 && g == 0);
     for (int i = gs; i < ge; ++i) op.row(b, i, slot0, li, acc);
-    publish_item<W, NS>(acc, b, r, R, partials, counters, colsum, s0, Kp);
+    publish_item<W, NS>(acc, b, r, R, partials, counters, colsum, s0, Kp, red);
   }
 }
 
@@ -348,14 +380,20 @@ struct PrimalOp {
 };
 
 template <int W, bool CHECK>
-__global__ void __launch_bounds__(kBlock) k_primal(Params P) {
-  const Ctrl C = *P.ctrl;
-  if (C.done) return;
+__device__ void primal_body(const Params& P, const Ctrl& C, double* red) {
   prof_begin(P, K_PRIMAL);
   PrimalOp<W, CHECK> op(P, C);
   const int nb = (C.active + W - 1) / W;
-  run_rows<W, 2>(op, P.n, nb, C.Rp, P.partials, P.counters, P.colsum, S_DX2, P.Kp);
+  run_rows<W, 2>(op, P.n, nb, C.Rp, P.partials, P.counters, P.colsum, S_DX2, P.Kp, red);
   prof_end(P, K_PRIMAL);
+}
+
+template <int W, bool CHECK>
+__global__ void __launch_bounds__(kBlock) k_primal(Params P) {
+  __shared__ double red[kRedDoubles];
+  const Ctrl C = *P.ctrl;
+  if (C.done) return;
+  primal_body<W, CHECK>(P, C, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -451,15 +489,21 @@ struct DualOp {
 };
 
 template <int W, bool CHECK>
-__global__ void __launch_bounds__(kBlock) k_dual(Params P) {
-  const Ctrl C = *P.ctrl;
-  if (C.done) return;
+__device__ void dual_body(const Params& P, const Ctrl& C, double* red) {
   prof_begin(P, K_DUAL);
   DualOp<W, CHECK> op(P, C);
   const int nb = (C.active + W - 1) / W;
   run_rows<W, DualOp<W, CHECK>::NS>(op, P.m, nb, C.Rd, P.partials, P.counters,
-                                    P.colsum, S_DY2, P.Kp);
+                                    P.colsum, S_DY2, P.Kp, red);
   prof_end(P, K_DUAL);
+}
+
+template <int W, bool CHECK>
+__global__ void __launch_bounds__(kBlock) k_dual(Params P) {
+  __shared__ double red[kRedDoubles];
+  const Ctrl C = *P.ctrl;
+  if (C.done) return;
+  dual_body<W, CHECK>(P, C, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -538,14 +582,20 @@ struct CheckOp {
 };
 
 template <int W>
-__global__ void __launch_bounds__(kBlock) k_check(Params P) {
-  const Ctrl C = *P.ctrl;
-  if (C.done || !C.check) return;
+__device__ void check_body(const Params& P, const Ctrl& C, double* red) {
   prof_begin(P, K_CHECK);
   CheckOp<W> op(P, C);
   const int nb = (C.active + W - 1) / W;
-  run_rows<W, 10>(op, P.n, nb, C.Rc, P.partials, P.counters, P.colsum, S_OBJ, P.Kp);
+  run_rows<W, 10>(op, P.n, nb, C.Rc, P.partials, P.counters, P.colsum, S_OBJ, P.Kp, red);
   prof_end(P, K_CHECK);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBlock) k_check(Params P) {
+  __shared__ double red[kRedDoubles];
+  const Ctrl C = *P.ctrl;
+  if (C.done || !C.check) return;
+  check_body<W>(P, C, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -582,14 +632,20 @@ struct CertOp {
 };
 
 template <int W>
-__global__ void __launch_bounds__(kBlock) k_cert(Params P) {
-  const Ctrl C = *P.ctrl;
-  if (C.done || !C.cert_pending) return;
+__device__ void cert_body(const Params& P, const Ctrl& C, double* red) {
   prof_begin(P, K_CERT);
   CertOp<W> op(P, C);
   const int nb = (C.active + W - 1) / W;
-  run_rows<W, 1>(op, P.n, nb, C.Rc, P.partials, P.counters, P.colsum, S_CERT, P.Kp);
+  run_rows<W, 1>(op, P.n, nb, C.Rc, P.partials, P.counters, P.colsum, S_CERT, P.Kp, red);
   prof_end(P, K_CERT);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBlock) k_cert(Params P) {
+  __shared__ double red[kRedDoubles];
+  const Ctrl C = *P.ctrl;
+  if (C.done || !C.cert_pending) return;
+  cert_body<W>(P, C, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -632,7 +688,8 @@ __global__ void __launch_bounds__(kBlock) k_spmm(Params P, int transpose,
   op.rows_out = transpose ? P.n : P.m;
   op.active = active;
   const int nb = (active + W - 1) / W;
-  run_rows<W, 1>(op, op.rows_out, nb, R, partials, counters, colsum, 0, P.Kp);
+  __shared__ double red[kRedDoubles];
+  run_rows<W, 1>(op, op.rows_out, nb, R, partials, counters, colsum, 0, P.Kp, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -803,19 +860,24 @@ __device__ __forceinline__ void set_cond(const Params& P,
 // for count <= 256, else strided per thread then a fixed tree.
 __device__ double ordered_sum(const double* v, int count, double* sh) {
   const int tid = threadIdx.x;
+  __shared__ double result;
   __syncthreads();
   if (count <= 256) {
+    if (tid < count) sh[tid] = v[tid];  // stage: one parallel load, then a
+    __syncthreads();                    // sequential sum out of shared memory
     if (tid == 0) {
       double s = 0.0;
-      for (int j = 0; j < count; ++j) s += v[j];
-      sh[0] = s;
+      for (int j = 0; j < count; ++j) s += sh[j];
+      result = s;
     }
+    __syncthreads();
+    return result;
   } else {
     double s = 0.0;
-    for (int j = tid; j < count; j += kDecideThreads) s += v[j];
+    for (int j = tid; j < count; j += (int)blockDim.x) s += v[j];
     sh[tid] = s;
     __syncthreads();
-    for (int off = kDecideThreads / 2; off > 0; off >>= 1) {
+    for (int off = (int)blockDim.x / 2; off > 0; off >>= 1) {
       if (tid < off) sh[tid] = sh[tid] + sh[tid + off];
       __syncthreads();
     }
@@ -857,17 +919,17 @@ __device__ void permute_slots(const Params& P, const int* perm, int width,
   constexpr int ND = 14;
   const int tid = threadIdx.x;
   for (int a = 0; a < ND; ++a) {
-    for (int s = tid; s < width; s += kDecideThreads) scratch[s] = darr[a][perm[s]];
+    for (int s = tid; s < width; s += (int)blockDim.x) scratch[s] = darr[a][perm[s]];
     __syncthreads();
-    for (int s = tid; s < width; s += kDecideThreads) darr[a][s] = scratch[s];
+    for (int s = tid; s < width; s += (int)blockDim.x) darr[a][s] = scratch[s];
     __syncthreads();
   }
   int* iarr[] = {P.slot_orig, P.has_best};
   int* iscratch = reinterpret_cast<int*>(scratch);
   for (int a = 0; a < 2; ++a) {
-    for (int s = tid; s < width; s += kDecideThreads) iscratch[s] = iarr[a][perm[s]];
+    for (int s = tid; s < width; s += (int)blockDim.x) iscratch[s] = iarr[a][perm[s]];
     __syncthreads();
-    for (int s = tid; s < width; s += kDecideThreads) iarr[a][s] = iscratch[s];
+    for (int s = tid; s < width; s += (int)blockDim.x) iarr[a][s] = iscratch[s];
     __syncthreads();
   }
 }
@@ -886,7 +948,7 @@ __device__ void finalize(const Params& P, Ctrl& C, double mean, double* sh,
   }
   __syncthreads();
   if (C.check) {
-    for (int j = tid; j < active0; j += kDecideThreads) {
+    for (int j = tid; j < active0; j += (int)blockDim.x) {
       const int v = P.verdict[j];
       int bits = 0;
       if (v == V_OPTIMAL || v == V_PRIMAL_INF || v == V_DUAL_INF) {
@@ -929,7 +991,7 @@ __device__ void finalize(const Params& P, Ctrl& C, double mean, double* sh,
   if (compact) {
     // swap-with-last compaction scan (batch_solver.hpp:273-278), simulated
     // on the slot permutation only; the arrays are permuted afterwards.
-    for (int s = tid; s < width; s += kDecideThreads) perm[s] = s;
+    for (int s = tid; s < width; s += (int)blockDim.x) perm[s] = s;
     __syncthreads();
     if (tid == 0) {
       int a = active0;
@@ -949,7 +1011,7 @@ __device__ void finalize(const Params& P, Ctrl& C, double mean, double* sh,
   }
   // iteration limit: freeze what is left from the best candidates (:280-295)
   if (at_cap && active > 0) {
-    for (int j = tid; j < active; j += kDecideThreads) {
+    for (int j = tid; j < active; j += (int)blockDim.x) {
       const int o = P.slot_orig[j];
       bl_column_result& r = P.res[o];
       r.status = BL_ITERATION_LIMIT;
@@ -976,7 +1038,7 @@ __device__ void finalize(const Params& P, Ctrl& C, double mean, double* sh,
   }
   // snapshot list (pre-compaction slots) and move list (post <- pre)
   if (C.check) {
-    for (int j = tid; j < active0; j += kDecideThreads) {
+    for (int j = tid; j < active0; j += (int)blockDim.x) {
       const int bits = snap_bits[j];
       if (bits) {
         const int k = atomicAdd(&n_snap, 1);
@@ -991,7 +1053,7 @@ __device__ void finalize(const Params& P, Ctrl& C, double mean, double* sh,
   if (compact && !(at_cap) && active > 0) {
     if (tid == 0) ish[1] = 0;
     __syncthreads();
-    for (int s = tid; s < active; s += kDecideThreads) {
+    for (int s = tid; s < active; s += (int)blockDim.x) {
       if (perm[s] != s) {
         const int k = atomicAdd(&ish[1], 1);
         P.moves[2 * k] = s;
@@ -1037,7 +1099,7 @@ __device__ void finalize(const Params& P, Ctrl& C, double mean, double* sh,
   const bool restart = ish[2] != 0;
   if (restart) {
     // gated weight update on the post-compaction active columns (:303-319)
-    for (int j = tid; j < active; j += kDecideThreads) {
+    for (int j = tid; j < active; j += (int)blockDim.x) {
       if (P.resid[j] <= P.anchor_resid[j]) {
         const double dxn = sqrt(cs(P, S_XA2, j));
         const double dyn = sqrt(cs(P, S_YA2, j));
@@ -1065,9 +1127,18 @@ __device__ void finalize(const Params& P, Ctrl& C, double mean, double* sh,
       C.alpha = (double)(C.inner_k + 1) / (double)(C.inner_k + 2);
       C.at_cap = C.total_k >= P.max_it;
       C.check = (C.total_k % P.period == 0) || C.at_cap;
+      const int nba = (C.active + P.W - 1) / P.W;
+      C.Rp = items_per_block(P.n, P.m, P.W, P.grid, nba, P.l2_budget);
+      C.Rd = items_per_block(P.m, P.n, P.W, P.grid, nba, P.l2_budget);
+      C.Rc = C.Rp;
     }
     C.cert_pending = 0;
-    set_cond(P, P.h_loop, C.done ? 0u : 1u);
+    // The graph loop hands the tail over to the persistent kernel once an
+    // iteration's streamed state is small enough to be latency-bound.
+    const double state_bytes =
+        8.0 * (double)((C.active + P.W - 1) / P.W) * P.W * (double)(P.n + P.m);
+    const bool handover = P.handover_bytes > 0.0 && state_bytes < P.handover_bytes;
+    set_cond(P, P.h_loop, (C.done || handover) ? 0u : 1u);
     set_cond(P, P.h_check, (!C.done && C.check) ? 1u : 0u);
     set_cond(P, P.h_snap, (C.n_snap > 0 || C.n_moves > 0) ? 1u : 0u);
     if (P.trace) set_cond(P, P.h_trace, C.hash_pending ? 1u : 0u);
@@ -1077,19 +1148,17 @@ __device__ void finalize(const Params& P, Ctrl& C, double mean, double* sh,
 // Folds the finished launches' entry/exit stamps into the accumulators and
 // credits this iteration's row kernels with their algorithmic bytes
 // (compulsory traffic, gathers counted once).
-__device__ void prof_fold(const Params& P, const Ctrl& C) {
-  if (!P.prof) return;
-  const unsigned long long now = gtime();
-  for (int k = 0; k < K_KINDS; ++k) {
-    const unsigned long long s = P.prof[2 * k], e = P.prof[2 * k + 1];
-    if (e != 0ull && s != ~0ull && e >= s) {
-      P.prof_acc[3 * k] += (double)(e - s);
-      P.prof_acc[3 * k + 1] += 1.0;
-    }
-    P.prof[2 * k] = ~0ull;
-    P.prof[2 * k + 1] = 0ull;
+// Called by the first K_KINDS threads (one kind each).
+__device__ void prof_fold(const Params& P, const Ctrl& C, int k, unsigned long long now) {
+  if (!P.prof || k >= K_KINDS) return;
+  const unsigned long long s = P.prof[2 * k], e = P.prof[2 * k + 1];
+  if (e != 0ull && s != ~0ull && e >= s) {
+    P.prof_acc[3 * k] += (double)(e - s);
+    P.prof_acc[3 * k + 1] += 1.0;
   }
-  P.prof[2 * K_DECIDE] = now;
+  P.prof[2 * k] = k == K_DECIDE ? now : ~0ull;
+  P.prof[2 * k + 1] = 0ull;
+  if (k != 0) return;
   const double n = P.n, m = P.m, nnz = (double)P.nnz, K = C.active;
   const double chk = C.check ? 1.0 : 0.0;
   P.prof_acc[3 * K_PRIMAL + 2] += 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 4.0 * n + chk * n);
@@ -1098,7 +1167,7 @@ __device__ void prof_fold(const Params& P, const Ctrl& C) {
     P.prof_acc[3 * K_CHECK + 2] += 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 5.0 * n);
 }
 
-__global__ void __launch_bounds__(kDecideThreads) k_decide(Params P, int phase) {
+__device__ void decide_body(const Params& P, int phase) {
   double* scratch = P.scratch;
   __shared__ double sh[kDecideThreads];
   __shared__ int ish[4];
@@ -1111,9 +1180,14 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(Params P, int phase) 
   const int active = C.active;
   double mean;
   if (phase == 0) {
+    if (tid < 32) {
+      unsigned long long now = 0;
+      if (tid == 0) now = gtime();
+      now = __shfl_sync(0xffffffffu, now, 0);
+      prof_fold(P, C, tid, now);
+    }
     if (tid == 0) {
       ish[3] = 0;
-      prof_fold(P, C);
       C.launches += 3 + (C.check ? 1 : 0);
       C.passes += 1;
       // a loop pass either advances total_k or is the single re-application
@@ -1121,7 +1195,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(Params P, int phase) 
       if (C.passes > 2 * P.max_it + 1024) ish[3] = 2;
     }
     __syncthreads();
-    for (int j = tid; j < active; j += kDecideThreads) {
+    for (int j = tid; j < active; j += (int)blockDim.x) {
       int err = 0;
       P.resid[j] = m_residual(cs(P, S_DX2, j), cs(P, S_DY2, j), cs(P, S_CROSS, j),
                               P.eta, P.w[j], &err);
@@ -1145,7 +1219,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(Params P, int phase) 
     const int count = P.avg_all ? P.width : active;
     mean = ordered_sum(P.resid, count, sh) / (double)count;
     if (C.inner_k == 0) {
-      for (int j = tid; j < active; j += kDecideThreads) P.anchor_resid[j] = P.resid[j];
+      for (int j = tid; j < active; j += (int)blockDim.x) P.anchor_resid[j] = P.resid[j];
     }
     if (tid == 0) {
       if (C.inner_k == 0) C.mean_anchor = mean;
@@ -1156,7 +1230,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(Params P, int phase) 
     }
     __syncthreads();
     if (C.check) {
-      for (int j = tid; j < active; j += kDecideThreads) {
+      for (int j = tid; j < active; j += (int)blockDim.x) {
         evaluate_column(P, j);
         int need = P.verdict[j] == V_CERT_NEED;
         if (!need && P.verdict[j] == V_NONE && dual_ray(P, j)) P.verdict[j] = V_DUAL_INF;
@@ -1179,7 +1253,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(Params P, int phase) 
     if (tid == 0) set_cond(P, P.h_cert, 0u);
   } else {
     mean = C.mean;
-    for (int j = tid; j < active; j += kDecideThreads) {
+    for (int j = tid; j < active; j += (int)blockDim.x) {
       if (P.verdict[j] != V_CERT_NEED) continue;
       const double res = sqrt(cs(P, S_CERT, j));
       if (res <= P.eps_infeas * fabs(P.t_dsup[j])) P.verdict[j] = V_PRIMAL_INF;
@@ -1200,8 +1274,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(Params P, int phase) 
 // ---------------------------------------------------------------------------
 // snapshots (vectors of finished / best / capped columns) and compaction
 // ---------------------------------------------------------------------------
-__global__ void k_snapshot(Params P) {
-  const Ctrl C = *P.ctrl;
+__device__ void snapshot_body(const Params& P, const Ctrl& C) {
   const int ns = C.n_snap;
   if (ns == 0) return;
   prof_begin(P, K_SNAPSHOT);
@@ -1253,8 +1326,7 @@ __global__ void k_snapshot(Params P) {
 // iteration the moved column's next iterate is recomputed from XT/YT/AXT of
 // the destination slot and its own pre-step iterate and anchor. On a
 // restart iteration (no Halpern) the current iterate is moved as is.
-__global__ void k_compact(Params P) {
-  const Ctrl C = *P.ctrl;
+__device__ void compact_body(const Params& P, const Ctrl& C) {
   const int nm = C.n_moves;
   if (nm == 0) return;
   prof_begin(P, K_COMPACT);
@@ -1303,7 +1375,7 @@ __global__ void k_compact(Params P) {
 
 // FNV-1a over the bytes of X[:,0] then Y[:,0] (solver.hpp:170-177,
 // batch_solver.hpp:339-344). Sequential by definition: one thread.
-__global__ void k_trace(Params P) {
+__device__ void trace_body(const Params& P) {
   Ctrl* C = P.ctrl;
   if (!C->hash_pending) return;
   uint64_t h = C->hash;
@@ -1325,6 +1397,96 @@ __global__ void k_trace(Params P) {
   }
   C->hash = h;
   C->hash_pending = 0;
+}
+
+__global__ void __launch_bounds__(kDecideThreads) k_decide(Params P, int phase) {
+  decide_body(P, phase);
+}
+__global__ void k_snapshot(Params P) {
+  const Ctrl C = *P.ctrl;
+  snapshot_body(P, C);
+}
+__global__ void k_compact(Params P) {
+  const Ctrl C = *P.ctrl;
+  compact_body(P, C);
+}
+__global__ void k_trace(Params P) { trace_body(P); }
+
+// ---------------------------------------------------------------------------
+// persistent loop: the whole solve in ONE cooperative launch
+// ---------------------------------------------------------------------------
+// All CTAs are co-resident (cooperative launch); phases are separated by a
+// grid barrier instead of kernel boundaries, CTA 0 runs the decide phase.
+// The gpu-scope fences of the barrier also invalidate L1, so gathers of data
+// written earlier in the launch see the new values.
+__device__ __forceinline__ void grid_sync(unsigned long long* bar, unsigned long long& target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1ull);
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ Ctrl load_ctrl(const Ctrl* c) {
+  static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl must be 8-byte sized");
+  Ctrl out;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(c);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(&out);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Ctrl) / 8); ++i) dst[i] = __ldcg(src + i);
+  return out;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBlock) k_loop(Params P) {
+  __shared__ double red[kRedDoubles];
+  unsigned long long target = 0;
+  for (;;) {
+    Ctrl C = load_ctrl(P.ctrl);
+    if (C.done) break;
+    if (C.check) {
+      primal_body<W, true>(P, C, red);
+      grid_sync(P.barrier, target);
+      dual_body<W, true>(P, C, red);
+      grid_sync(P.barrier, target);
+      check_body<W>(P, C, red);
+      grid_sync(P.barrier, target);
+    } else {
+      primal_body<W, false>(P, C, red);
+      grid_sync(P.barrier, target);
+      dual_body<W, false>(P, C, red);
+      grid_sync(P.barrier, target);
+    }
+    if (blockIdx.x == 0) decide_body(P, 0);
+    grid_sync(P.barrier, target);
+    C = load_ctrl(P.ctrl);
+    if (C.cert_pending) {
+      cert_body<W>(P, C, red);
+      grid_sync(P.barrier, target);
+      if (blockIdx.x == 0) decide_body(P, 1);
+      grid_sync(P.barrier, target);
+      C = load_ctrl(P.ctrl);
+    }
+    if (C.n_snap > 0 || C.n_moves > 0) {
+      snapshot_body(P, C);
+      grid_sync(P.barrier, target);
+      compact_body(P, C);
+      grid_sync(P.barrier, target);
+    }
+    if (C.hash_pending) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) trace_body(P);
+      grid_sync(P.barrier, target);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1416,7 +1578,8 @@ __global__ void __launch_bounds__(kBlock) k_pi_spmv(Params P, int transpose,
     any = any || op.valid[v];
   }
   if (!any) return;
-  run_rows<2, 1>(op, op.rows_out, 1, R, partials, counters, colsum, 0, 2);
+  __shared__ double red[kRedDoubles];
+  run_rows<2, 1>(op, op.rows_out, 1, R, partials, counters, colsum, 0, 2, red);
 }
 
 // stage 0 (after u = A v): null-space test; stage 1 (after w = A'u):
@@ -1525,19 +1688,57 @@ void launch_spmm(const Params& P, cudaStream_t s, bool transpose, const double* 
   });
 }
 
+// Each row kernel is launched with SMs x (its own max resident CTAs, <= 4):
+// the grid-stride item loop does not depend on the grid size.
+static int grid_of(const void* fn) {
+  static std::mutex mu;
+  static std::map<const void*, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(fn);
+  if (it != cache.end()) return it->second;
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, 0);
+  if (occ < 1) occ = 1;
+  if (occ > 4) occ = 4;
+  return cache[fn] = sms * occ;
+}
+
 void launch_iteration_check(const Params& P, cudaStream_t s) {
   BL_DISPATCH_W(P.W, {
-    k_primal<W_, true><<<P.grid, kBlock, 0, s>>>(P);
-    k_dual<W_, true><<<P.grid, kBlock, 0, s>>>(P);
-    k_check<W_><<<P.grid, kBlock, 0, s>>>(P);
+    k_primal<W_, true><<<grid_of((const void*)k_primal<W_, true>), kBlock, 0, s>>>(P);
+    k_dual<W_, true><<<grid_of((const void*)k_dual<W_, true>), kBlock, 0, s>>>(P);
+    k_check<W_><<<grid_of((const void*)k_check<W_>), kBlock, 0, s>>>(P);
   });
 }
 
 void launch_iteration_plain(const Params& P, cudaStream_t s) {
   BL_DISPATCH_W(P.W, {
-    k_primal<W_, false><<<P.grid, kBlock, 0, s>>>(P);
-    k_dual<W_, false><<<P.grid, kBlock, 0, s>>>(P);
+    k_primal<W_, false><<<grid_of((const void*)k_primal<W_, false>), kBlock, 0, s>>>(P);
+    k_dual<W_, false><<<grid_of((const void*)k_dual<W_, false>), kBlock, 0, s>>>(P);
   });
+}
+
+// CTAs per SM the persistent loop kernel can keep co-resident.
+int loop_ctas_per_sm(int W) {
+  int occ = 1;
+  BL_DISPATCH_W(W, {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_loop<W_>, kBlock, 0);
+  });
+  return occ < 1 ? 1 : occ;
+}
+
+// The whole solve as one cooperative launch (P.grid co-resident CTAs).
+cudaError_t launch_loop(const Params& P, cudaStream_t s) {
+  Params Q = P;
+  void* args[] = {&Q};
+  cudaError_t e = cudaSuccess;
+  BL_DISPATCH_W(P.W, {
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_loop<W_>),
+                                    dim3(P.grid), dim3(kBlock), args, 0, s);
+  });
+  return e;
 }
 
 void launch_decide(const Params& P, cudaStream_t s, int phase) {

@@ -85,13 +85,15 @@ struct bl_ctx {
   cudaStream_t stream = nullptr, side = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int grid = 148;
+  int sms = 148;
+  long long l2_bytes = 126ll << 20;
   std::string err;
   // workspace
   enum {
     B_X0, B_X1, B_Y0, B_Y1, B_AX0, B_AX1, B_aX, B_aY, B_aAX, B_XT, B_YT, B_DY,
     B_RC, B_R, B_DR, B_AXT, B_BX, B_BY, B_BR, B_RX, B_RY, B_RR, B_RDX, B_RDY, B_RDR,
     B_SLOTD, B_SLOTI, B_ORIGI, B_RES, B_COLSUM, B_PART, B_CNT, B_SNAP, B_MOVES,
-    B_LOG, B_CTRL, B_PROF, B_PROFACC, B_OV, B_OVD, B_WARMX, B_WARMY, B_PI, B_TMP0, B_TMP1, B_COUNT
+    B_LOG, B_CTRL, B_PROF, B_PROFACC, B_BAR, B_OV, B_OVD, B_WARMX, B_WARMY, B_PI, B_TMP0, B_TMP1, B_COUNT
   };
   DevBuf buf[B_COUNT];
   // last solve
@@ -546,10 +548,42 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.res = static_cast<bl_column_result*>(
       ctx->buf[bl_ctx::B_RES].ensure(sizeof(bl_column_result) * (size_t)width));
   P.colsum = static_cast<double*>(ctx->buf[bl_ctx::B_COLSUM].ensure(sizeof(double) * bl::S_COUNT * (size_t)Kp));
-  const int Rp = items_for(n, W, ctx->grid), Rd = items_for(m, W, ctx->grid);
-  const int Rmax = std::max(Rp, Rd);
+  // loop driver: one cooperative persistent launch (default), the CUDA
+  // graph with conditional nodes, or host-stepped kernels (debugging)
+  // 0 auto: the graph loop while an iteration streams more than
+  //   kHandoverBytes of state (bandwidth-bound; separately compiled kernels
+  //   run at higher occupancy), then the persistent kernel for the
+  //   latency-bound tail; 1 graph only; 2 host-stepped; 3 persistent only.
+  constexpr double kHandoverBytes = 16.0 * (1 << 20);
+  int mode_loop = 0;
+  if (const char* e = std::getenv("BATCHLP_LOOP")) {
+    if (std::strcmp(e, "graph") == 0) mode_loop = 1;
+    else if (std::strcmp(e, "step") == 0) mode_loop = 2;
+    else if (std::strcmp(e, "persistent") == 0) mode_loop = 3;
+  }
+  if (const char* e = std::getenv("BATCHLP_STEP_MODE"))
+    if (e[0] == '1') mode_loop = 2;
+  const int grid = ctx->grid;
+  int occ_loop = bl::loop_ctas_per_sm(W);
+  if (occ_loop > 4) occ_loop = 4;
+  const int grid_loop = ctx->sms * occ_loop;
+  const double state0 = 8.0 * (double)nb * W * (double)(n + m);
+  const bool use_graph = mode_loop == 1 || mode_loop == 2 ||
+                         (mode_loop == 0 && state0 >= kHandoverBytes);
+  const bool use_loop = mode_loop == 3 || mode_loop == 0;
+  const long long l2_budget = ctx->l2_bytes / 2;
+  // partials: the largest (active blocks x items per block) any iteration
+  // uses, under either driver's grid
+  size_t max_items = 1;
+  for (int g : {grid, grid_loop}) {
+    for (int nba = 1; nba <= nb; ++nba) {
+      const size_t a = (size_t)nba * bl::items_per_block(n, m, W, g, nba, l2_budget);
+      const size_t b = (size_t)nba * bl::items_per_block(m, n, W, g, nba, l2_budget);
+      max_items = std::max(max_items, std::max(a, b));
+    }
+  }
   P.partials = static_cast<double*>(
-      ctx->buf[bl_ctx::B_PART].ensure(sizeof(double) * (size_t)nb * Rmax * 10 * W));
+      ctx->buf[bl_ctx::B_PART].ensure(sizeof(double) * max_items * 10 * W));
   P.counters = static_cast<int*>(ctx->buf[bl_ctx::B_CNT].ensure(sizeof(int) * (size_t)std::max(nb, 64)));
   P.snap_list = static_cast<int*>(ctx->buf[bl_ctx::B_SNAP].ensure(sizeof(int) * 3 * (size_t)Kp));
   P.moves = static_cast<int*>(ctx->buf[bl_ctx::B_MOVES].ensure(sizeof(int) * 2 * (size_t)Kp));
@@ -602,7 +636,12 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.avg_all = cfg.average_over_all_columns != 0;
   P.trace = cfg.trace_iterates != 0;
   P.vectors = vec;
-  P.grid = ctx->grid;
+  P.grid = use_graph ? grid : grid_loop;
+  P.l2_budget = l2_budget;
+  P.handover_bytes = (mode_loop == 0) ? kHandoverBytes : 0.0;
+  P.barrier = static_cast<unsigned long long*>(
+      ctx->buf[bl_ctx::B_BAR].ensure(sizeof(unsigned long long)));
+  ck(cudaMemsetAsync(P.barrier, 0, sizeof(unsigned long long), s), "barrier");
 
   // ---- host-side initial state ----
   {
@@ -649,16 +688,30 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   c0.at_cap = 0 >= cfg.max_iterations;
   c0.check = 1;
   c0.anchor_reset = 1;
-  c0.Rp = Rp;
-  c0.Rd = Rd;
-  c0.Rc = Rp;
+  {
+    const int nba = (active + W - 1) / W;
+    c0.Rp = bl::items_per_block(n, m, W, P.grid, nba, l2_budget);
+    c0.Rd = bl::items_per_block(m, n, W, P.grid, nba, l2_budget);
+    c0.Rc = c0.Rp;
+  }
   *ctx->h_ctrl = c0;
   ck(cudaMemcpyAsync(P.ctrl, ctx->h_ctrl, sizeof(bl::Ctrl), cudaMemcpyHostToDevice, s), "ctrl");
 
   if (active > 0) {
-    const char* step = std::getenv("BATCHLP_STEP_MODE");
-    if (step && step[0] == '1') run_loop_steps(ctx, P);
-    else run_loop_graph(ctx, P);
+    if (mode_loop == 2) {
+      run_loop_steps(ctx, P);
+    } else {
+      if (use_graph) run_loop_graph(ctx, P);
+      if (use_loop) {
+        // continues from the control block wherever the graph stopped (a
+        // no-op launch when the graph already finished the batch)
+        bl::Params Q = P;
+        Q.grid = grid_loop;
+        Q.handover_bytes = 0.0;
+        Q.use_graph = 0;
+        ck(bl::launch_loop(Q, s), "cooperative loop launch");
+      }
+    }
   }
   ck(cudaGetLastError(), "loop launch");
   ck(cudaMemcpyAsync(ctx->h_ctrl, P.ctrl, sizeof(bl::Ctrl), cudaMemcpyDeviceToHost, s), "ctrl");
@@ -767,6 +820,10 @@ int bl_ctx_create(int device, bl_ctx** out) {
     int occ = bl::max_ctas_per_sm();
     if (occ > 4) occ = 4;
     ctx->grid = sms * occ;
+    ctx->sms = sms;
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
+    if (l2 > 0) ctx->l2_bytes = l2;
   });
   if (rc != BL_OK) {
     delete ctx;
