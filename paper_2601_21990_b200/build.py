@@ -69,6 +69,20 @@ def build_oracles(verbose: bool = False) -> None:
     subprocess.run(cmd, check=True)
 
 
+def build_cpp_tests(verbose: bool = False) -> None:
+    """tests/cpp/Makefile: our C++ drop-in tests always; the reference's own
+    unit suites compiled against our headers only where /root/reference
+    exists (the GPU box runs the prebuilt binary)."""
+    targets = ["dropin"]
+    if os.path.isdir("/root/reference/proj/tests"):
+        targets.append("ref")
+    cmd = ["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp"), *targets]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+
+
 if __name__ == "__main__":
     build_library(force="--force" in sys.argv, verbose=True)
     build_oracles(verbose=True)
+    build_cpp_tests(verbose=True)
