@@ -11,7 +11,9 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libbatchlp_cuda.so")
+# BATCHLP_LIB selects an alternative in-tree build (tuning variants under
+# lib/variants/); it is still this package's CUDA library, never a fallback.
+LIB_PATH = os.environ.get("BATCHLP_LIB") or os.path.join(_HERE, "lib", "libbatchlp_cuda.so")
 
 # enum values (batchlp_cuda.h)
 BL_OK = 0

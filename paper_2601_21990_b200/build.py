@@ -55,6 +55,19 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(tag: str, defines, verbose: bool = False) -> str:
+    """A tuning variant of the library (extra -D flags) under lib/variants/,
+    selected at run time with BATCHLP_LIB (scripts/ tuning sweeps)."""
+    out = os.path.join(LIBDIR, "variants", f"libbatchlp_cuda_{tag}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+           *[os.path.join(CSRC, s) for s in SOURCES], "-o", out]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True, cwd=CSRC)
+    return out
+
+
 def build_oracles(verbose: bool = False) -> None:
     """oracle/Makefile: the C restatement always; the reference shim only
     where /root/reference exists (the GPU box uses the prebuilt .so)."""

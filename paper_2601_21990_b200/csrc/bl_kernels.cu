@@ -231,6 +231,18 @@ __device__ __forceinline__ void publish_item(double (&acc)[NS][Geo<W>::V], int b
   __syncthreads();
 }
 
+// Column descriptor of one LP slot as staged in shared memory (ColInfo).
+struct SColInfo {
+  int valid, orig, ob, oe, v0, k0;
+  double val0, step;
+};
+
+// Resident CTAs per SM the row kernels are compiled for (caps registers).
+#ifndef BL_ROW_MIN_CTAS
+#define BL_ROW_MIN_CTAS 3
+#endif
+constexpr int kRowMinCtas = BL_ROW_MIN_CTAS;
+
 // Walks the work items of a persistent row kernel. Op provides:
 //   begin(b, slot0, acc, owner)  per item (owner: holds the matrix's row 0)
 //   row(b, i, slot0, acc)        per row of the group's contiguous chunk
@@ -240,6 +252,7 @@ __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
                                          double* colsum, int s0, int Kp, double* red) {
   using Gm = Geo<W>;
   constexpr int V = Gm::V, L = Gm::L, G = Gm::G;
+  __shared__ SColInfo s_col[W];
   const int tid = threadIdx.x, g = tid / L, li = tid - g * L;
   const int items = nb * R;
   const int per = R > 0 ? (rows + R - 1) / R : 0;
@@ -262,7 +275,9 @@ __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
 #pragma unroll
       for (int v = 0; v < V; ++v) acc[s][v] = 0.0;
     const int slot0 = b * W + li * V;
-    op.begin(b, slot0, acc, r == 0 && g == 0);
+    if (tid < W) op.stage(b * W + tid, &s_col[tid]);
+    __syncthreads();
+    op.begin(b, slot0, acc, r == 0 && g == 0, &s_col[li * V]);
     for (int i = gs; i < ge; ++i) op.row(b, i, slot0, li, acc);
     publish_item<W, NS>(acc, b, r, R, partials, counters, colsum, s0, Kp, red);
   }
@@ -317,6 +332,36 @@ __device__ __forceinline__ void col_vals(const Params& P, const ColInfo& c, int 
     if (P.ov_var[k] == i) apply_ov(P.ov_kind[k], P.ov_val[k], cc, lo, hi);
 }
 
+// The column descriptors of the block a CTA is working on live in shared
+// memory (staged once per work item) and are re-read per row through a
+// volatile view, so they do not occupy registers across the gather loop:
+// register pressure, not bandwidth, sets the occupancy of the row kernels.
+__device__ __forceinline__ ColInfo read_col(const volatile SColInfo* s) {
+  ColInfo c;
+  c.valid = s->valid;
+  c.orig = s->orig;
+  c.ob = s->ob;
+  c.oe = s->oe;
+  c.v0 = s->v0;
+  c.k0 = s->k0;
+  c.val0 = s->val0;
+  c.step = s->step;
+  return c;
+}
+__device__ __forceinline__ void stage_col(const Params& P, int j, int active, bool dual_step,
+                                          volatile SColInfo* s) {
+  ColInfo c;
+  load_col(P, j, active, dual_step, c);
+  s->valid = c.valid;
+  s->orig = c.orig;
+  s->ob = c.ob;
+  s->oe = c.oe;
+  s->v0 = c.v0;
+  s->k0 = c.k0;
+  s->val0 = c.val0;
+  s->step = c.step;
+}
+
 // ---------------------------------------------------------------------------
 // primal: XT = proj(X - tau (c + A'Y)), X' = Halpern, sums
 // ---------------------------------------------------------------------------
@@ -328,7 +373,7 @@ struct PrimalOp {
   double alpha, oma;
   const double *Ycur, *Xcur;
   double* Xnxt;
-  ColInfo col[V];
+  const volatile SColInfo* col;  // this lane's V column descriptors (shared memory)
   __device__ PrimalOp(const Params& p, const Ctrl& C) : P(p) {
     active = C.active;
     reset = C.anchor_reset;
@@ -338,14 +383,13 @@ struct PrimalOp {
     Xcur = P.X[C.cur];
     Xnxt = P.X[C.cur ^ 1];
   }
-  __device__ void begin(int, int slot0, double (&)[2][V], bool) {
-#pragma unroll
-    for (int v = 0; v < V; ++v) load_col(P, slot0 + v, active, false, col[v]);
+  __device__ void stage(int j, volatile SColInfo* s) { stage_col(P, j, active, false, s); }
+  __device__ void begin(int, int, double (&)[2][V], bool, const volatile SColInfo* sc) {
+    col = sc;
   }
   __device__ void row(int b, int i, int, int li, double (&acc)[2][V]) {
     const int n = P.n, m = P.m;
-    double aty[V];
-    gather_row<W>(P.trp, P.tci, P.tcv, Ycur + (size_t)b * m * W + li * V, i, aty);
+    // streamed operands first, so their latency overlaps the gathers
     const double bc = P.mode == BL_SHARED_OBJECTIVE ? __ldg(P.c + i) : 0.0;
     const double bl = __ldg(P.xl + i), bh = __ldg(P.xu + i);
     const size_t idx = ((size_t)b * n + i) * W + li * V;
@@ -357,15 +401,18 @@ struct PrimalOp {
     } else {
       ld_cs<V>(P.aX + idx, ax);
     }
+    double aty[V];
+    gather_row<W>(P.trp, P.tci, P.tcv, Ycur + (size_t)b * m * W + li * V, i, aty);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
+      const ColInfo cl = read_col(col + v);
       double cc, lo, hi;
-      col_vals(P, col[v], i, bc, bl, bh, cc, lo, hi);
+      col_vals(P, cl, i, bc, bl, bh, cc, lo, hi);
       const double t = cc + aty[v];
-      xt[v] = project_box(x[v] - col[v].step * t, lo, hi);
+      xt[v] = project_box(x[v] - cl.step * t, lo, hi);
       const double dx = xt[v] - x[v];
       const double da = x[v] - ax[v];
-      if (col[v].valid) {
+      if (cl.valid) {
         acc[0][v] += dx * dx;
         acc[1][v] += da * da;
       }
@@ -389,7 +436,7 @@ __device__ void primal_body(const Params& P, const Ctrl& C, double* red) {
 }
 
 template <int W, bool CHECK>
-__global__ void __launch_bounds__(kBlock) k_primal(Params P) {
+__global__ void __launch_bounds__(kBlock, kRowMinCtas) k_primal(Params P) {
   __shared__ double red[kRedDoubles];
   const Ctrl C = *P.ctrl;
   if (C.done) return;
@@ -408,7 +455,7 @@ struct DualOp {
   double alpha, oma;
   const double *Ycur, *AXcur;
   double *Ynxt, *AXnxt;
-  ColInfo col[V];
+  const volatile SColInfo* col;
   __device__ DualOp(const Params& p, const Ctrl& C) : P(p) {
     active = C.active;
     reset = C.anchor_reset;
@@ -419,14 +466,12 @@ struct DualOp {
     Ynxt = P.Y[C.cur ^ 1];
     AXnxt = P.AX[C.cur ^ 1];
   }
-  __device__ void begin(int, int slot0, double (&)[NS][V], bool) {
-#pragma unroll
-    for (int v = 0; v < V; ++v) load_col(P, slot0 + v, active, true, col[v]);
+  __device__ void stage(int j, volatile SColInfo* s) { stage_col(P, j, active, true, s); }
+  __device__ void begin(int, int, double (&)[NS][V], bool, const volatile SColInfo* sc) {
+    col = sc;
   }
   __device__ void row(int b, int i, int, int li, double (&acc)[NS][V]) {
     const int n = P.n, m = P.m;
-    double axt[V];
-    gather_row<W>(P.rp, P.ci, P.cv, P.XT + (size_t)b * n * W + li * V, i, axt);
     const double lo = __ldg(P.rl + i), hi = __ldg(P.ru + i);
     const size_t idx = ((size_t)b * m + i) * W + li * V;
     double y[V], ax[V], ay[V], aax[V], yt[V], yn[V], axn[V], dyb[V];
@@ -442,16 +487,19 @@ struct DualOp {
       ld_cs<V>(P.aY + idx, ay);
       ld_cs<V>(P.aAX + idx, aax);
     }
+    double axt[V];
+    gather_row<W>(P.rp, P.ci, P.cv, P.XT + (size_t)b * n * W + li * V, i, axt);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const double sigma = col[v].step;
+      const ColInfo cl = read_col(col + v);
+      const double sigma = cl.step;
       // dual_step_element, solver.hpp:186-190
       const double vv = 2.0 * axt[v] - ax[v];
       const double s = y[v] / sigma + vv;
       yt[v] = sigma * (s - project_box(s, lo, hi));
       const double dy = yt[v] - y[v];
       const double da = y[v] - ay[v];
-      if (col[v].valid) {
+      if (cl.valid) {
         acc[0][v] += dy * dy;
         acc[1][v] += dy * (axt[v] - ax[v]);
         acc[2][v] += da * da;
@@ -460,7 +508,7 @@ struct DualOp {
       axn[v] = alpha * (2.0 * axt[v] - ax[v]) + oma * aax[v];
       if constexpr (CHECK) {
         dyb[v] = project_barrier(yt[v] - y[v], lo, hi);
-        if (col[v].valid) {
+        if (cl.valid) {
           acc[3][v] += support_term(yt[v], lo, hi);
           const double viol = axt[v] - project_box(axt[v], lo, hi);
           acc[4][v] += viol * viol;
@@ -499,7 +547,7 @@ __device__ void dual_body(const Params& P, const Ctrl& C, double* red) {
 }
 
 template <int W, bool CHECK>
-__global__ void __launch_bounds__(kBlock) k_dual(Params P) {
+__global__ void __launch_bounds__(kBlock, kRowMinCtas) k_dual(Params P) {
   __shared__ double red[kRedDoubles];
   const Ctrl C = *P.ctrl;
   if (C.done) return;
@@ -516,15 +564,17 @@ struct CheckOp {
   const Params& P;
   int active;
   const double* Xcur;
-  ColInfo col[V];
+  const volatile SColInfo* col;
   __device__ CheckOp(const Params& p, const Ctrl& C) : P(p) {
     active = C.active;
     Xcur = P.X[C.cur];
   }
-  __device__ void begin(int, int slot0, double (&acc)[NS][V], bool owner) {
+  __device__ void stage(int j, volatile SColInfo* s) { stage_col(P, j, active, false, s); }
+  __device__ void begin(int, int slot0, double (&acc)[NS][V], bool owner,
+                        const volatile SColInfo* sc) {
+    col = sc;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      load_col(P, slot0 + v, active, false, col[v]);
       // The displacement support of the probe continues the row-space sum
       // (solver.hpp:463-474): seed it into the chunk holding variable 0.
       if (owner && col[v].valid) {
@@ -535,8 +585,6 @@ struct CheckOp {
   }
   __device__ void row(int b, int i, int, int li, double (&acc)[NS][V]) {
     const int n = P.n, m = P.m;
-    double atyt[V];
-    gather_row<W>(P.trp, P.tci, P.tcv, P.YT + (size_t)b * m * W + li * V, i, atyt);
     const double bc = P.mode == BL_SHARED_OBJECTIVE ? __ldg(P.c + i) : 0.0;
     const double bl = __ldg(P.xl + i), bh = __ldg(P.xu + i);
     const size_t idx = ((size_t)b * n + i) * W + li * V;
@@ -544,16 +592,19 @@ struct CheckOp {
     ld_cg<V>(P.XT + idx, xt);
     ld_cs<V>(Xcur + idx, x);
     ld_cs<V>(P.RC + idx, rc);
+    double atyt[V];
+    gather_row<W>(P.trp, P.tci, P.tcv, P.YT + (size_t)b * m * W + li * V, i, atyt);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
+      const ColInfo cl = read_col(col + v);
       double cc, lo, hi;
-      col_vals(P, col[v], i, bc, bl, bh, cc, lo, hi);
+      col_vals(P, cl, i, bc, bl, bh, cc, lo, hi);
       // evaluate_optimality, solver.hpp:369-386
       const double g = -cc - atyt[v];
       r[v] = project_barrier(g, lo, hi);
       // check_infeasibility_probe, solver.hpp:454-456
       dr[v] = project_barrier(r[v] - rc[v], lo, hi);
-      if (col[v].valid) {
+      if (cl.valid) {
         acc[0][v] += cc * xt[v];
         acc[1][v] += cc * cc;
         const double viol = cc + atyt[v] + r[v];
@@ -591,7 +642,7 @@ __device__ void check_body(const Params& P, const Ctrl& C, double* red) {
 }
 
 template <int W>
-__global__ void __launch_bounds__(kBlock) k_check(Params P) {
+__global__ void __launch_bounds__(kBlock, kRowMinCtas) k_check(Params P) {
   __shared__ double red[kRedDoubles];
   const Ctrl C = *P.ctrl;
   if (C.done || !C.check) return;
@@ -608,7 +659,8 @@ struct CertOp {
   int active;
   int flag[V];
   __device__ CertOp(const Params& p, const Ctrl& C) : P(p) { active = C.active; }
-  __device__ void begin(int, int slot0, double (&)[1][V], bool) {
+  __device__ void stage(int, volatile SColInfo*) {}
+  __device__ void begin(int, int slot0, double (&)[1][V], bool, const volatile SColInfo*) {
 #pragma unroll
     for (int v = 0; v < V; ++v)
       flag[v] = (slot0 + v < active) ? P.cert_flag[slot0 + v] : 0;
@@ -641,7 +693,7 @@ __device__ void cert_body(const Params& P, const Ctrl& C, double* red) {
 }
 
 template <int W>
-__global__ void __launch_bounds__(kBlock) k_cert(Params P) {
+__global__ void __launch_bounds__(kBlock, kRowMinCtas) k_cert(Params P) {
   __shared__ double red[kRedDoubles];
   const Ctrl C = *P.ctrl;
   if (C.done || !C.cert_pending) return;
@@ -659,7 +711,8 @@ struct SpmmOp {
   double* out;
   int rows_in, rows_out, active;
   int valid[V];
-  __device__ void begin(int, int slot0, double (&)[1][V], bool) {
+  __device__ void stage(int, volatile SColInfo*) {}
+  __device__ void begin(int, int slot0, double (&)[1][V], bool, const volatile SColInfo*) {
 #pragma unroll
     for (int v = 0; v < V; ++v) valid[v] = slot0 + v < active;
   }
@@ -1446,45 +1499,71 @@ __device__ __forceinline__ Ctrl load_ctrl(const Ctrl* c) {
   return out;
 }
 
-template <int W>
+// One thread-block cluster: phases separated by the hardware cluster
+// barrier (release/acquire at cluster scope; it also invalidates L1, so the
+// gathers see data other CTAs of the cluster wrote in the previous phase).
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// CL = false: cooperative grid over all SMs (grid barriers); it hands over
+// (returns) once at most P.tail_blocks column blocks are active.
+// CL = true: ONE cluster of P.grid CTAs for the latency-bound tail, where an
+// iteration is a few microseconds of work and a grid-wide barrier would cost
+// more than the work itself.
+template <int W, bool CL>
 __global__ void __launch_bounds__(kBlock) k_loop(Params P) {
   __shared__ double red[kRedDoubles];
   unsigned long long target = 0;
+  auto sync = [&]() {
+    if constexpr (CL) cluster_sync_all();
+    else grid_sync(P.barrier, target);
+  };
+  const int grid = gridDim.x;
   for (;;) {
     Ctrl C = load_ctrl(P.ctrl);
     if (C.done) break;
+    const int nba = (C.active + W - 1) / W;
+    if (!CL && P.tail_blocks > 0 && nba <= P.tail_blocks) break;
+    // work decomposition for THIS launch's grid (the control block may have
+    // been written by a driver with another grid)
+    C.Rp = items_per_block(P.n, P.m, W, grid, nba, P.l2_budget);
+    C.Rd = items_per_block(P.m, P.n, W, grid, nba, P.l2_budget);
+    C.Rc = C.Rp;
     if (C.check) {
       primal_body<W, true>(P, C, red);
-      grid_sync(P.barrier, target);
+      sync();
       dual_body<W, true>(P, C, red);
-      grid_sync(P.barrier, target);
+      sync();
       check_body<W>(P, C, red);
-      grid_sync(P.barrier, target);
+      sync();
     } else {
       primal_body<W, false>(P, C, red);
-      grid_sync(P.barrier, target);
+      sync();
       dual_body<W, false>(P, C, red);
-      grid_sync(P.barrier, target);
+      sync();
     }
     if (blockIdx.x == 0) decide_body(P, 0);
-    grid_sync(P.barrier, target);
+    sync();
     C = load_ctrl(P.ctrl);
     if (C.cert_pending) {
+      C.Rc = items_per_block(P.n, P.m, W, grid, (C.active + W - 1) / W, P.l2_budget);
       cert_body<W>(P, C, red);
-      grid_sync(P.barrier, target);
+      sync();
       if (blockIdx.x == 0) decide_body(P, 1);
-      grid_sync(P.barrier, target);
+      sync();
       C = load_ctrl(P.ctrl);
     }
     if (C.n_snap > 0 || C.n_moves > 0) {
       snapshot_body(P, C);
-      grid_sync(P.barrier, target);
+      sync();
       compact_body(P, C);
-      grid_sync(P.barrier, target);
+      sync();
     }
     if (C.hash_pending) {
       if (blockIdx.x == 0 && threadIdx.x == 0) trace_body(P);
-      grid_sync(P.barrier, target);
+      sync();
     }
   }
 }
@@ -1545,7 +1624,8 @@ struct PiOp {
   double* out;
   int rows_in, rows_out;
   int valid[2];
-  __device__ void begin(int, int, double (&)[1][2], bool) {}
+  __device__ void stage(int, volatile SColInfo*) {}
+  __device__ void begin(int, int, double (&)[1][2], bool, const volatile SColInfo*) {}
   __device__ void row(int, int i, int, int, double (&acc)[1][2]) {
     double o[2];
     gather_row<2>(rp, ci, cv, in, i, o);
@@ -1724,21 +1804,80 @@ void launch_iteration_plain(const Params& P, cudaStream_t s) {
 int loop_ctas_per_sm(int W) {
   int occ = 1;
   BL_DISPATCH_W(W, {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_loop<W_>, kBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_loop<W_, false>, kBlock, 0);
   });
   return occ < 1 ? 1 : occ;
 }
 
-// The whole solve as one cooperative launch (P.grid co-resident CTAs).
+// The whole solve (or its remainder) as one cooperative launch of P.grid
+// co-resident CTAs.
 cudaError_t launch_loop(const Params& P, cudaStream_t s) {
   Params Q = P;
   void* args[] = {&Q};
   cudaError_t e = cudaSuccess;
   BL_DISPATCH_W(P.W, {
-    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_loop<W_>),
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_loop<W_, false>),
                                     dim3(P.grid), dim3(kBlock), args, 0, s);
   });
   return e;
+}
+
+// The tail as ONE thread-block cluster of P.grid CTAs (<= 16; sizes above
+// 8 need the non-portable-cluster opt-in).
+cudaError_t launch_loop_cluster(const Params& P, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  BL_DISPATCH_W(P.W, {
+    auto fn = k_loop<W_, true>;
+    if (P.grid > 8) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P.grid);
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P.grid;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, fn, P);
+  });
+  return e;
+}
+
+// Largest cluster (<= 16) of the tail kernel the device can place (cached).
+int max_tail_cluster(int W) {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(W);
+  if (it != cache.end()) return it->second;
+  int best = 8;
+  BL_DISPATCH_W(W, {
+    auto fn = k_loop<W_, true>;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+        cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(16);
+      cfg.blockDim = dim3(kBlock);
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 16;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int clusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) == cudaSuccess && clusters > 0)
+        best = 16;
+    }
+  });
+  cudaGetLastError();
+  cache[W] = best;
+  return best;
 }
 
 void launch_decide(const Params& P, cudaStream_t s, int phase) {

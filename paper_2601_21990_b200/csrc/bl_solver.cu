@@ -553,14 +553,23 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   // 0 auto: the graph loop while an iteration streams more than
   //   kHandoverBytes of state (bandwidth-bound; separately compiled kernels
   //   run at higher occupancy), then the persistent kernel for the
-  //   latency-bound tail; 1 graph only; 2 host-stepped; 3 persistent only.
+  //   latency-bound rest, then (<= tail_blocks active column blocks) one
+  //   thread-block cluster for the last few LPs; 1 graph only;
+  //   2 host-stepped; 3 persistent grid + cluster; 4 cluster only.
   constexpr double kHandoverBytes = 16.0 * (1 << 20);
   int mode_loop = 0;
   if (const char* e = std::getenv("BATCHLP_LOOP")) {
     if (std::strcmp(e, "graph") == 0) mode_loop = 1;
     else if (std::strcmp(e, "step") == 0) mode_loop = 2;
     else if (std::strcmp(e, "persistent") == 0) mode_loop = 3;
+    else if (std::strcmp(e, "cluster") == 0) mode_loop = 4;
   }
+  int tail_blocks = 1;
+  if (const char* e = std::getenv("BATCHLP_TAIL_BLOCKS")) tail_blocks = std::atoi(e);
+  int tail_cluster = bl::max_tail_cluster(W);
+  if (const char* e = std::getenv("BATCHLP_TAIL_CLUSTER")) tail_cluster = std::atoi(e);
+  if (tail_cluster < 1) tail_cluster = 1;
+  if (tail_cluster > 16) tail_cluster = 16;
   if (const char* e = std::getenv("BATCHLP_STEP_MODE"))
     if (e[0] == '1') mode_loop = 2;
   const int grid = ctx->grid;
@@ -571,11 +580,16 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   const bool use_graph = mode_loop == 1 || mode_loop == 2 ||
                          (mode_loop == 0 && state0 >= kHandoverBytes);
   const bool use_loop = mode_loop == 3 || mode_loop == 0;
-  const long long l2_budget = ctx->l2_bytes / 2;
+  const bool use_cluster = (mode_loop == 0 || mode_loop == 3) ? tail_blocks > 0 : mode_loop == 4;
+  // Gathered-operand bytes kept in flight (tuned on B200:
+  // fewer blocks in flight raise the L2 hit rate of the gathers);
+  // overridable for tuning sweeps.
+  long long l2_budget = 16ll << 20;
+  if (const char* e = std::getenv("BATCHLP_L2_BUDGET_MB")) l2_budget = std::atoll(e) << 20;
   // partials: the largest (active blocks x items per block) any iteration
   // uses, under either driver's grid
   size_t max_items = 1;
-  for (int g : {grid, grid_loop}) {
+  for (int g : {grid, grid_loop, tail_cluster}) {
     for (int nba = 1; nba <= nb; ++nba) {
       const size_t a = (size_t)nba * bl::items_per_block(n, m, W, g, nba, l2_budget);
       const size_t b = (size_t)nba * bl::items_per_block(m, n, W, g, nba, l2_budget);
@@ -709,7 +723,18 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
         Q.grid = grid_loop;
         Q.handover_bytes = 0.0;
         Q.use_graph = 0;
+        Q.tail_blocks = use_cluster ? tail_blocks : 0;
         ck(bl::launch_loop(Q, s), "cooperative loop launch");
+      }
+      if (use_cluster) {
+        // the last few LPs: one cluster, hardware barriers (no-op when the
+        // batch is already finished)
+        bl::Params Q = P;
+        Q.grid = tail_cluster;
+        Q.handover_bytes = 0.0;
+        Q.use_graph = 0;
+        Q.tail_blocks = 0;
+        ck(bl::launch_loop_cluster(Q, s), "cluster loop launch");
       }
     }
   }

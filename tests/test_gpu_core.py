@@ -106,3 +106,23 @@ def test_c1_strong_branching_matches_reference(ref):
                      (br.down_iterations, want["down_iterations"][j])):
             assert abs(g - w) <= 0.1 * w
     assert abs(got.iterations - want["iterations"]) <= 0.1 * want["iterations"]
+
+
+@pytest.mark.parametrize("loop", ["graph", "persistent", "cluster", "step"])
+def test_loop_drivers_agree_with_reference_c1(ref, loop, monkeypatch):
+    """Every loop driver (CUDA graph with conditional nodes, cooperative
+    persistent grid, single thread-block cluster, host-stepped) runs the same
+    device control logic: C1 strong branching matches the reference."""
+    monkeypatch.setenv("BATCHLP_LOOP", loop)
+    p = I.config_problem("c1")
+    root = ref.solve(p).per_problem[0]
+    frac = I.pick_fractional(root.x, 16)
+    got = bl.run_fsb(bl.FsbRequest(p, root.x, frac))
+    want = ref.run_fsb(p, root.x, frac)
+    for j, br in enumerate(got.branches):
+        assert int(br.up_status) == want["up_status"][j]
+        assert int(br.down_status) == want["down_status"][j]
+        assert abs(br.up_objective - want["up_objective"][j]) <= 1e-6 * (1 + abs(want["up_objective"][j]))
+        assert abs(br.down_objective - want["down_objective"][j]) <= 1e-6 * (1 + abs(want["down_objective"][j]))
+        assert abs(br.up_iterations - want["up_iterations"][j]) <= 0.1 * want["up_iterations"][j]
+        assert abs(br.down_iterations - want["down_iterations"][j]) <= 0.1 * want["down_iterations"][j]
