@@ -16,15 +16,17 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libbatchlp_cuda.so")
-SOURCES = ["bl_kernels.cu", "bl_solver.cu", "bl_generators.cpp"]
-HEADERS = ["bl_device.cuh"]
+SOURCES = ["bl_kernels.cu", "bl_w1.cu", "bl_w2.cu", "bl_w4.cu", "bl_w8.cu", "bl_w16.cu",
+           "bl_w32.cu", "bl_solver.cu", "bl_generators.cpp"]
+HEADERS = ["bl_device.cuh", "bl_kernels.cuh"]
 
+# compile flags (objects) and link flags (the shared library)
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
     "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
-    "-shared",
 ]
+LINK_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared"]
 
 
 def _nvcc() -> str:
@@ -39,19 +41,46 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _compile_all(defines, objdir, verbose):
+    """nvcc -c of every source in parallel (one translation unit per kernel
+    width); returns the object paths."""
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(objdir, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include")]
+
+    def one(src):
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS]
+        deps.append(os.path.join(ROOT, "include", "batchlp_cuda.h"))
+        if _stale(obj, deps):
+            cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], *inc, "-c",
+                   os.path.join(CSRC, src), "-o", obj + ".tmp"]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            subprocess.run(cmd, check=True, cwd=CSRC)
+            os.replace(obj + ".tmp", obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        return list(ex.map(one, SOURCES))
+
+
+def _link(objs, out, verbose):
+    cmd = [_nvcc(), *LINK_FLAGS, *objs, "-o", out + ".tmp"]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True, cwd=CSRC)
+    os.replace(out + ".tmp", out)
+
+
 def build_library(force: bool = False, verbose: bool = False) -> str:
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "batchlp_cuda.h"))
     if not force and not _stale(LIB, deps):
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"),
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True, cwd=CSRC)
-    os.replace(tmp, LIB)
+    objs = _compile_all([], os.path.join(HERE, "build", "obj"), verbose)
+    _link(objs, LIB, verbose)
     return LIB
 
 
@@ -60,11 +89,8 @@ def build_variant(tag: str, defines, verbose: bool = False) -> str:
     selected at run time with BATCHLP_LIB (scripts/ tuning sweeps)."""
     out = os.path.join(LIBDIR, "variants", f"libbatchlp_cuda_{tag}.so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", out]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True, cwd=CSRC)
+    objs = _compile_all(defines, os.path.join(HERE, "build", f"obj_{tag}"), verbose)
+    _link(objs, out, verbose)
     return out
 
 

@@ -1,0 +1,2151 @@
+// bl_kernels.cuh — sm_100a device code of the batched PDHG hot path.
+//
+// Templates and device functions shared by the translation units: the
+// per-width kernel instantiations (bl_w*.cu, built in parallel) and the
+// width-independent kernels and launchers (bl_kernels.cu).
+//
+// One solver iteration (reference batch_solver.hpp:174-345) is three launches
+// on plain iterations and up to seven on termination-check iterations:
+//
+//   k_primal<W,CHECK>  ATY = A'Y fused with the primal projection, the
+//                      speculative Halpern step for X and the per-column
+//                      sums sum dx^2, sum (x - anchor_x)^2   (:176-187,:326-330)
+//   k_dual<W,CHECK>    AXT = A XT fused with the dual step, the speculative
+//                      Halpern step for Y and AX and the per-column sums of
+//                      the M-norm residual (:188-208); on check iterations
+//                      also every row-space term of evaluate_optimality and
+//                      of the infeasibility probe (solver.hpp:387-396,448-514)
+//   k_check<W>         AT_YT = A'YT fused with the reduced costs and every
+//                      column-space term of the check (:226-272)
+//   k_decide           one CTA: residuals, averaged residual, statuses,
+//                      best-candidate offers, swap-with-last compaction, the
+//                      restart rule and weight update (:209-324)
+//   k_cert<W>          masked A'dy for columns whose certificate needs it
+//   k_snapshot, k_compact   vector snapshots and state column moves
+//
+// "Speculative Halpern": the kernels write z' = alpha (2 T(z) - z) +
+// (1 - alpha) z0 into the second buffer of a double-buffered X/Y/AX while
+// they compute T(z); the decide kernel either flips the buffer (no restart)
+// or keeps the old one (a restart re-applies T at the same point,
+// batch_solver.hpp:320-322). So a restart costs nothing and anchor copies
+// are fused into the next iteration's reads.
+//
+// The row kernels are persistent: a fixed grid of CTAs walks work items
+// (column block b, row range r) in block-major order so the gathered operand
+// of one 32-column block stays L2 resident while all SMs work on it.
+// Per-column sums are reduced deterministically: sequentially within a row
+// group, then a fixed tree, then the last CTA of each block folds the
+// per-item partials in item order. Items of <= kTinyRows rows are walked by a
+// single group, so on small problems every sum is the reference's sequential
+// sum, bit for bit.
+
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <map>
+#include <mutex>
+
+#include "bl_device.cuh"
+
+namespace bl {
+
+// ---------------------------------------------------------------------------
+// geometry and vector memory helpers
+// ---------------------------------------------------------------------------
+// LL > 0: "narrow" mapping for the latency-bound tail, where only the first
+// LL * V slots of the (single) active block are live: fewer lanes per row,
+// more rows processed in parallel. The tiled layout (stride W) is unchanged.
+template <int W, int LL = 0>
+struct Geo {
+  static constexpr int V = W >= 2 ? 2 : 1;                      // slots per lane (double2)
+  static constexpr int L = LL > 0 ? LL : (W >= 2 ? W / 2 : 1);  // lanes per row
+  static constexpr int G = kBlock / L;                          // row groups per CTA
+};
+
+template <int V>
+__device__ __forceinline__ void ld_nc(const double* p, double (&o)[V]) {
+  if constexpr (V == 2) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    o[0] = t.x;
+    o[1] = t.y;
+  } else {
+    o[0] = __ldg(p);
+  }
+}
+// streamed once per iteration: evict-first so gathered tiles keep the L2
+template <int V>
+__device__ __forceinline__ void ld_cs(const double* p, double (&o)[V]) {
+  if constexpr (V == 2) {
+    const double2 t = __ldcs(reinterpret_cast<const double2*>(p));
+    o[0] = t.x;
+    o[1] = t.y;
+  } else {
+    o[0] = __ldcs(p);
+  }
+}
+template <int V>
+__device__ __forceinline__ void ld_cg(const double* p, double (&o)[V]) {
+  if constexpr (V == 2) {
+    const double2 t = __ldcg(reinterpret_cast<const double2*>(p));
+    o[0] = t.x;
+    o[1] = t.y;
+  } else {
+    o[0] = __ldcg(p);
+  }
+}
+template <int V>
+__device__ __forceinline__ void st_cs(double* p, const double (&v)[V]) {
+  if constexpr (V == 2) {
+    __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+  } else {
+    __stcs(p, v[0]);
+  }
+}
+template <int V>
+__device__ __forceinline__ void st_wb(double* p, const double (&v)[V]) {
+  if constexpr (V == 2) {
+    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  } else {
+    *p = v[0];
+  }
+}
+
+// One CSR row of op(A) times the lane's V slots of a column block. The
+// accumulation follows the stored order with separately rounded products
+// and sums: the reference csr_apply (sparse.hpp:176-183) bit for bit.
+template <int W, bool GENERIC = false>
+__device__ __forceinline__ void gather_row(const int* __restrict__ rp,
+                                           const int* __restrict__ ci,
+                                           const double* __restrict__ cv,
+                                           const double* __restrict__ base,
+                                           int i, double (&acc)[Geo<W>::V]) {
+  constexpr int V = Geo<W>::V;
+  // GENERIC: the row metadata may live in shared memory (the tail's CSR
+  // cache), so it is read with generic loads instead of the read-only path.
+  auto ldi = [](const int* q) { return GENERIC ? *q : __ldg(q); };
+  auto ldd = [](const double* q) { return GENERIC ? *q : __ldg(q); };
+  int p = ldi(rp + i);
+  const int e = ldi(rp + i + 1);
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.0;
+  for (; p + 4 <= e; p += 4) {
+    const int c0 = ldi(ci + p), c1 = ldi(ci + p + 1);
+    const int c2 = ldi(ci + p + 2), c3 = ldi(ci + p + 3);
+    const double a0 = ldd(cv + p), a1 = ldd(cv + p + 1);
+    const double a2 = ldd(cv + p + 2), a3 = ldd(cv + p + 3);
+    double x0[V], x1[V], x2[V], x3[V];
+    ld_nc<V>(base + (size_t)c0 * W, x0);
+    ld_nc<V>(base + (size_t)c1 * W, x1);
+    ld_nc<V>(base + (size_t)c2 * W, x2);
+    ld_nc<V>(base + (size_t)c3 * W, x3);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      acc[v] = __dadd_rn(acc[v], __dmul_rn(a0, x0[v]));
+      acc[v] = __dadd_rn(acc[v], __dmul_rn(a1, x1[v]));
+      acc[v] = __dadd_rn(acc[v], __dmul_rn(a2, x2[v]));
+      acc[v] = __dadd_rn(acc[v], __dmul_rn(a3, x3[v]));
+    }
+  }
+  for (; p < e; ++p) {
+    const int c0 = ldi(ci + p);
+    const double a0 = ldd(cv + p);
+    double x0[V];
+    ld_nc<V>(base + (size_t)c0 * W, x0);
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = __dadd_rn(acc[v], __dmul_rn(a0, x0[v]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// deterministic per-column reduction of one work item
+// ---------------------------------------------------------------------------
+// acc[s][v]: this lane's sums for slots (b*W + li*V + v). Reduces over the
+// CTA in a fixed tree, writes the item's partials, and the last CTA of block
+// b folds all R partials in item order into colsum[s0+s][slot].
+// `red` is a shared buffer of at least kRedDoubles doubles.
+template <int W, int NS, int LL = 0>
+__device__ __forceinline__ void publish_item(double (&acc)[NS][Geo<W>::V], int b,
+                                             int r, int R, double* partials,
+                                             int* counters, double* colsum,
+                                             int s0, int Kp, double* red) {
+  using Gm = Geo<W, LL>;
+  constexpr int V = Gm::V, L = Gm::L;
+  static_assert(kWarps * NS * W <= kRedDoubles, "reduction buffer too small");
+  __shared__ int last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int off = 16; off >= L; off >>= 1) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        acc[s][v] = __dadd_rn(acc[s][v], __shfl_down_sync(0xffffffffu, acc[s][v], off));
+  }
+  if (lane < L) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int v = 0; v < V; ++v) red[(warp * NS + s) * W + lane * V + v] = acc[s][v];
+  }
+  __syncthreads();
+  for (int t = tid; t < NS * W; t += kBlock) {
+    const int s = t / W, jj = t - s * W;
+    double sum = 0.0;
+    if (jj < L * V) {  // slots beyond a narrow mapping's lanes are not live
+#pragma unroll
+      for (int wp = 0; wp < kWarps; ++wp) sum = __dadd_rn(sum, red[(wp * NS + s) * W + jj]);
+    }
+    partials[((size_t)(b * R + r) * NS + s) * W + jj] = sum;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = (atomicAdd(&counters[b], 1) == R - 1);
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    constexpr int Q = NS * W;  // outputs of this block
+    if constexpr (Q <= kBlock) {
+      // T threads per output; thread `part` folds items part, part+T, ...
+      // in order, then the T partial folds are added in part order. Fixed
+      // order for any timing; with R = 1 it is the single partial exactly.
+      double* fold = red;  // free again: the item partials are written
+      constexpr int T = kBlock / Q;
+      const int q = tid % Q, part = tid / Q;
+      double sum = 0.0;
+      if (part < T) {
+        const int s = q / W, jj = q - s * W;
+        const double* src = partials + ((size_t)b * R * NS + s) * W + jj;
+#pragma unroll 8
+        for (int rr = part; rr < R; rr += T)
+          sum = __dadd_rn(sum, __ldcg(src + (size_t)rr * NS * W));
+      }
+      fold[tid] = sum;
+      __syncthreads();
+      if (tid < Q) {
+        double tot = 0.0;
+#pragma unroll
+        for (int pp = 0; pp < T; ++pp) tot = __dadd_rn(tot, fold[pp * Q + tid]);
+        const int s = tid / W, jj = tid - s * W;
+        colsum[(size_t)(s0 + s) * Kp + b * W + jj] = tot;
+      }
+    } else {
+      for (int t = tid; t < Q; t += kBlock) {
+        const int s = t / W, jj = t - s * W;
+        const double* src = partials + ((size_t)b * R * NS + s) * W + jj;
+        double sum = 0.0;
+#pragma unroll 8
+        for (int rr = 0; rr < R; ++rr) sum = __dadd_rn(sum, __ldcg(src + (size_t)rr * NS * W));
+        colsum[(size_t)(s0 + s) * Kp + b * W + jj] = sum;
+      }
+    }
+    if (tid == 0) counters[b] = 0;
+  }
+  __syncthreads();
+}
+
+// Column descriptor of one LP slot as staged in shared memory (ColInfo).
+struct SColInfo {
+  int valid, orig, ob, oe, v0, k0;
+  double val0, step;
+};
+
+// One shared array of column descriptors per CTA, whichever run_rows
+// instantiation uses it (a __shared__ in a non-template function has a
+// single instance).
+static __device__ __noinline__ SColInfo* col_smem() {
+  __shared__ SColInfo s[32];
+  return s;
+}
+
+// Resident CTAs per SM the row kernels are compiled for (caps registers).
+#ifndef BL_ROW_MIN_CTAS
+#define BL_ROW_MIN_CTAS 3
+#endif
+constexpr int kRowMinCtas = BL_ROW_MIN_CTAS;
+
+// Walks the work items of a persistent row kernel. Op provides:
+//   begin(b, slot0, acc, owner)  per item (owner: holds the matrix's row 0)
+//   row(b, i, slot0, acc)        per row of the group's contiguous chunk
+template <int W, int NS, int LL = 0, class Op>
+__device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
+                                         double* partials, int* counters,
+                                         double* colsum, int s0, int Kp, double* red) {
+  using Gm = Geo<W, LL>;
+  constexpr int V = Gm::V, L = Gm::L, G = Gm::G;
+  SColInfo* s_col = col_smem();
+  const int tid = threadIdx.x, g = tid / L, li = tid - g * L;
+  const int items = nb * R;
+  const int per = R > 0 ? (rows + R - 1) / R : 0;
+  for (int w = blockIdx.x; w < items; w += gridDim.x) {
+    const int b = w / R, r = w - b * R;
+    const int r0 = min(rows, r * per), r1 = min(rows, r0 + per);
+    const int cnt = r1 - r0;
+    int gs, ge;
+    if (rows <= kTinyRows) {  // whole dimension tiny: one sequential walk
+      gs = g == 0 ? r0 : r1;
+      ge = r1;
+    } else {
+      const int ch = (cnt + G - 1) / G;
+      gs = min(r1, r0 + g * ch);
+      ge = min(r1, gs + ch);
+    }
+    double acc[NS][V];
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[s][v] = 0.0;
+    const int slot0 = b * W + li * V;
+    if (tid < W) op.stage(b * W + tid, &s_col[tid]);
+    __syncthreads();
+    op.begin(b, slot0, acc, r == 0 && g == 0, &s_col[li * V]);
+    for (int i = gs; i < ge; ++i) op.row(b, i, slot0, li, acc);
+    publish_item<W, NS, LL>(acc, b, r, R, partials, counters, colsum, s0, Kp, red);
+  }
+}
+
+// Effective cost / bounds of one column at one variable (ColumnView,
+// problem.hpp:209-236): base entry or signed unit objective, then the
+// column's overrides in list order (later entries win).
+struct ColInfo {
+  int valid, orig, ob, oe, v0, k0;
+  double val0, step;
+};
+
+__device__ __forceinline__ void load_col(const Params& P, int j, int active,
+                                         bool dual_step, ColInfo& c) {
+  c.valid = j < active;
+  c.orig = c.valid ? P.slot_orig[j] : 0;
+  c.ob = c.valid ? P.ov_beg[c.orig] : 0;
+  c.oe = c.valid ? P.ov_end[c.orig] : 0;
+  c.v0 = -1;
+  c.k0 = 0;
+  c.val0 = 0.0;
+  if (c.oe > c.ob) {
+    c.v0 = P.ov_var[c.ob];
+    c.k0 = P.ov_kind[c.ob];
+    c.val0 = P.ov_val[c.ob];
+  }
+  // StepParams (solver.hpp:58-59): tau = eta / w, sigma = eta * w
+  const double w = c.valid ? P.w[j] : 1.0;
+  c.step = dual_step ? P.eta * w : P.eta / w;
+}
+
+__device__ __forceinline__ void apply_ov(int kind, double val, double& cc,
+                                         double& lo, double& hi) {
+  if (kind == BL_OVERRIDE_OBJECTIVE) cc = val;
+  else if (kind == BL_OVERRIDE_LOWER) lo = val;
+  else hi = val;
+}
+
+__device__ __forceinline__ void col_vals(const Params& P, const ColInfo& c, int i,
+                                         double bc, double bl, double bh,
+                                         double& cc, double& lo, double& hi) {
+  cc = bc;
+  lo = bl;
+  hi = bh;
+  if (P.mode == BL_SIGNED_UNIT_COLUMNS) {
+    const int n = P.n;
+    cc = c.orig < n ? (i == c.orig ? 1.0 : 0.0) : (i == c.orig - n ? -1.0 : 0.0);
+  }
+  if (c.v0 == i) apply_ov(c.k0, c.val0, cc, lo, hi);
+  for (int k = c.ob + 1; k < c.oe; ++k)
+    if (P.ov_var[k] == i) apply_ov(P.ov_kind[k], P.ov_val[k], cc, lo, hi);
+}
+
+// The column descriptors of the block a CTA is working on live in shared
+// memory (staged once per work item) and are re-read per row through a
+// volatile view, so they do not occupy registers across the gather loop:
+// register pressure, not bandwidth, sets the occupancy of the row kernels.
+__device__ __forceinline__ ColInfo read_col(const volatile SColInfo* s) {
+  ColInfo c;
+  c.valid = s->valid;
+  c.orig = s->orig;
+  c.ob = s->ob;
+  c.oe = s->oe;
+  c.v0 = s->v0;
+  c.k0 = s->k0;
+  c.val0 = s->val0;
+  c.step = s->step;
+  return c;
+}
+__device__ __forceinline__ void stage_col(const Params& P, int j, int active, bool dual_step,
+                                          volatile SColInfo* s) {
+  ColInfo c;
+  load_col(P, j, active, dual_step, c);
+  s->valid = c.valid;
+  s->orig = c.orig;
+  s->ob = c.ob;
+  s->oe = c.oe;
+  s->v0 = c.v0;
+  s->k0 = c.k0;
+  s->val0 = c.val0;
+  s->step = c.step;
+}
+
+// ---------------------------------------------------------------------------
+// primal: XT = proj(X - tau (c + A'Y)), X' = Halpern, sums
+// ---------------------------------------------------------------------------
+template <int W, bool CHECK>
+struct PrimalOp {
+  static constexpr int V = Geo<W>::V;
+  const Params& P;
+  int active, reset;
+  double alpha, oma;
+  const double *Ycur, *Xcur;
+  double* Xnxt;
+  const volatile SColInfo* col;  // this lane's V column descriptors (shared memory)
+  const int* crp;                // A' CSR (global, or a shared-memory cache of it)
+  const int* cci;
+  const double* ccv;
+  bool cached = false;
+  __device__ PrimalOp(const Params& p, const Ctrl& C) : P(p) {
+    crp = P.trp;
+    cci = P.tci;
+    ccv = P.tcv;
+    active = C.active;
+    reset = C.anchor_reset;
+    alpha = C.alpha;
+    oma = 1.0 - alpha;
+    Ycur = P.Y[C.cur];
+    Xcur = P.X[C.cur];
+    Xnxt = P.X[C.cur ^ 1];
+  }
+  __device__ void stage(int j, volatile SColInfo* s) { stage_col(P, j, active, false, s); }
+  __device__ void begin(int, int, double (&)[2][V], bool, const volatile SColInfo* sc) {
+    col = sc;
+  }
+  __device__ void row(int b, int i, int, int li, double (&acc)[2][V]) {
+    const int n = P.n, m = P.m;
+    // streamed operands first, so their latency overlaps the gathers
+    const double bc = P.mode == BL_SHARED_OBJECTIVE ? __ldg(P.c + i) : 0.0;
+    const double bl = __ldg(P.xl + i), bh = __ldg(P.xu + i);
+    const size_t idx = ((size_t)b * n + i) * W + li * V;
+    double x[V], ax[V], xt[V], xn[V], rc[V];
+    ld_cs<V>(Xcur + idx, x);
+    if (reset) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) ax[v] = x[v];
+    } else {
+      ld_cs<V>(P.aX + idx, ax);
+    }
+    double aty[V];
+    if (cached) gather_row<W, true>(crp, cci, ccv, Ycur + (size_t)b * m * W + li * V, i, aty);
+    else gather_row<W>(crp, cci, ccv, Ycur + (size_t)b * m * W + li * V, i, aty);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const ColInfo cl = read_col(col + v);
+      double cc, lo, hi;
+      col_vals(P, cl, i, bc, bl, bh, cc, lo, hi);
+      const double t = cc + aty[v];
+      xt[v] = project_box(x[v] - cl.step * t, lo, hi);
+      const double dx = xt[v] - x[v];
+      const double da = x[v] - ax[v];
+      if (cl.valid) {
+        acc[0][v] += dx * dx;
+        acc[1][v] += da * da;
+      }
+      xn[v] = alpha * (2.0 * xt[v] - x[v]) + oma * ax[v];
+      if (CHECK) rc[v] = project_barrier(-cc - aty[v], lo, hi);
+    }
+    st_wb<V>(P.XT + idx, xt);
+    st_cs<V>(Xnxt + idx, xn);
+    if (reset) st_cs<V>(P.aX + idx, x);
+    if (CHECK) st_wb<V>(P.RC + idx, rc);
+  }
+};
+
+template <int W, bool CHECK, int LL = 0>
+static __device__ void primal_body(const Params& P, const Ctrl& C, double* red) {
+  prof_begin(P, K_PRIMAL);
+  PrimalOp<W, CHECK> op(P, C);
+  const int nb = (C.active + W - 1) / W;
+  run_rows<W, 2, LL>(op, P.n, nb, C.Rp, P.partials, P.counters, P.colsum, S_DX2, P.Kp, red);
+  prof_end(P, K_PRIMAL);
+}
+
+template <int W, bool CHECK>
+__global__ void __launch_bounds__(kBlock, kRowMinCtas) k_primal(Params P) {
+  __shared__ double red[kRedDoubles];
+  const Ctrl C = *P.ctrl;
+  if (C.done) return;
+  primal_body<W, CHECK>(P, C, red);
+}
+
+// ---------------------------------------------------------------------------
+// dual: AXT = A XT, YT = sigma (s - proj(s)), Y'/AX' = Halpern, sums
+// ---------------------------------------------------------------------------
+template <int W, bool CHECK>
+struct DualOp {
+  static constexpr int V = Geo<W>::V;
+  static constexpr int NS = CHECK ? 9 : 3;
+  const Params& P;
+  int active, reset;
+  double alpha, oma;
+  const double *Ycur, *AXcur;
+  double *Ynxt, *AXnxt;
+  const volatile SColInfo* col;
+  const int* crp;  // A CSR (global, or a shared-memory cache of it)
+  const int* cci;
+  const double* ccv;
+  bool cached = false;
+  __device__ DualOp(const Params& p, const Ctrl& C) : P(p) {
+    crp = P.rp;
+    cci = P.ci;
+    ccv = P.cv;
+    active = C.active;
+    reset = C.anchor_reset;
+    alpha = C.alpha;
+    oma = 1.0 - alpha;
+    Ycur = P.Y[C.cur];
+    AXcur = P.AX[C.cur];
+    Ynxt = P.Y[C.cur ^ 1];
+    AXnxt = P.AX[C.cur ^ 1];
+  }
+  __device__ void stage(int j, volatile SColInfo* s) { stage_col(P, j, active, true, s); }
+  __device__ void begin(int, int, double (&)[NS][V], bool, const volatile SColInfo* sc) {
+    col = sc;
+  }
+  __device__ void row(int b, int i, int, int li, double (&acc)[NS][V]) {
+    const int n = P.n, m = P.m;
+    const double lo = __ldg(P.rl + i), hi = __ldg(P.ru + i);
+    const size_t idx = ((size_t)b * m + i) * W + li * V;
+    double y[V], ax[V], ay[V], aax[V], yt[V], yn[V], axn[V], dyb[V];
+    ld_cs<V>(Ycur + idx, y);
+    ld_cs<V>(AXcur + idx, ax);
+    if (reset) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        ay[v] = y[v];
+        aax[v] = ax[v];
+      }
+    } else {
+      ld_cs<V>(P.aY + idx, ay);
+      ld_cs<V>(P.aAX + idx, aax);
+    }
+    double axt[V];
+    if (cached) gather_row<W, true>(crp, cci, ccv, P.XT + (size_t)b * n * W + li * V, i, axt);
+    else gather_row<W>(crp, cci, ccv, P.XT + (size_t)b * n * W + li * V, i, axt);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const ColInfo cl = read_col(col + v);
+      const double sigma = cl.step;
+      // dual_step_element, solver.hpp:186-190
+      const double vv = 2.0 * axt[v] - ax[v];
+      const double s = y[v] / sigma + vv;
+      yt[v] = sigma * (s - project_box(s, lo, hi));
+      const double dy = yt[v] - y[v];
+      const double da = y[v] - ay[v];
+      if (cl.valid) {
+        acc[0][v] += dy * dy;
+        acc[1][v] += dy * (axt[v] - ax[v]);
+        acc[2][v] += da * da;
+      }
+      yn[v] = alpha * (2.0 * yt[v] - y[v]) + oma * ay[v];
+      axn[v] = alpha * (2.0 * axt[v] - ax[v]) + oma * aax[v];
+      if constexpr (CHECK) {
+        dyb[v] = project_barrier(yt[v] - y[v], lo, hi);
+        if (cl.valid) {
+          acc[3][v] += support_term(yt[v], lo, hi);
+          const double viol = axt[v] - project_box(axt[v], lo, hi);
+          acc[4][v] += viol * viol;
+          acc[5][v] += axt[v] * axt[v];
+          const double term = support_term(dyb[v], lo, hi);
+          acc[6][v] += term;
+          acc[7][v] += fabs(term);
+          const double adx = axt[v] - ax[v];
+          const double rv = adx - project_recession(adx, lo, hi);
+          acc[8][v] += rv * rv;
+        }
+      }
+    }
+    st_cs<V>(Ynxt + idx, yn);
+    st_cs<V>(AXnxt + idx, axn);
+    if (reset) {
+      st_cs<V>(P.aY + idx, y);
+      st_cs<V>(P.aAX + idx, ax);
+    }
+    if constexpr (CHECK) {
+      st_wb<V>(P.YT + idx, yt);
+      st_wb<V>(P.AXT + idx, axt);
+      st_wb<V>(P.DY + idx, dyb);
+    }
+  }
+};
+
+template <int W, bool CHECK, int LL = 0>
+static __device__ void dual_body(const Params& P, const Ctrl& C, double* red) {
+  prof_begin(P, K_DUAL);
+  DualOp<W, CHECK> op(P, C);
+  const int nb = (C.active + W - 1) / W;
+  run_rows<W, DualOp<W, CHECK>::NS, LL>(op, P.m, nb, C.Rd, P.partials, P.counters,
+                                    P.colsum, S_DY2, P.Kp, red);
+  prof_end(P, K_DUAL);
+}
+
+template <int W, bool CHECK>
+__global__ void __launch_bounds__(kBlock, kRowMinCtas) k_dual(Params P) {
+  __shared__ double red[kRedDoubles];
+  const Ctrl C = *P.ctrl;
+  if (C.done) return;
+  dual_body<W, CHECK>(P, C, red);
+}
+
+// ---------------------------------------------------------------------------
+// check: AT_YT = A'YT, reduced costs and the column-space check terms
+// ---------------------------------------------------------------------------
+template <int W>
+struct CheckOp {
+  static constexpr int V = Geo<W>::V;
+  static constexpr int NS = 10;
+  const Params& P;
+  int active;
+  const double* Xcur;
+  const volatile SColInfo* col;
+  __device__ CheckOp(const Params& p, const Ctrl& C) : P(p) {
+    active = C.active;
+    Xcur = P.X[C.cur];
+  }
+  __device__ void stage(int j, volatile SColInfo* s) { stage_col(P, j, active, false, s); }
+  __device__ void begin(int, int slot0, double (&acc)[NS][V], bool owner,
+                        const volatile SColInfo* sc) {
+    col = sc;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      // The displacement support of the probe continues the row-space sum
+      // (solver.hpp:463-474): seed it into the chunk holding variable 0.
+      if (owner && col[v].valid) {
+        acc[5][v] = P.colsum[(size_t)S_DYSUP * P.Kp + slot0 + v];
+        acc[6][v] = P.colsum[(size_t)S_DYSCALE * P.Kp + slot0 + v];
+      }
+    }
+  }
+  __device__ void row(int b, int i, int, int li, double (&acc)[NS][V]) {
+    const int n = P.n, m = P.m;
+    const double bc = P.mode == BL_SHARED_OBJECTIVE ? __ldg(P.c + i) : 0.0;
+    const double bl = __ldg(P.xl + i), bh = __ldg(P.xu + i);
+    const size_t idx = ((size_t)b * n + i) * W + li * V;
+    double xt[V], x[V], rc[V], r[V], dr[V];
+    ld_cg<V>(P.XT + idx, xt);
+    ld_cs<V>(Xcur + idx, x);
+    ld_cs<V>(P.RC + idx, rc);
+    double atyt[V];
+    gather_row<W>(P.trp, P.tci, P.tcv, P.YT + (size_t)b * m * W + li * V, i, atyt);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const ColInfo cl = read_col(col + v);
+      double cc, lo, hi;
+      col_vals(P, cl, i, bc, bl, bh, cc, lo, hi);
+      // evaluate_optimality, solver.hpp:369-386
+      const double g = -cc - atyt[v];
+      r[v] = project_barrier(g, lo, hi);
+      // check_infeasibility_probe, solver.hpp:454-456
+      dr[v] = project_barrier(r[v] - rc[v], lo, hi);
+      if (cl.valid) {
+        acc[0][v] += cc * xt[v];
+        acc[1][v] += cc * cc;
+        const double viol = cc + atyt[v] + r[v];
+        acc[2][v] += viol * viol;
+        if (P.robust) {
+          if (g > 0.0 && hi != kInf) acc[3][v] += hi * g;
+          else if (g < 0.0 && lo != -kInf) acc[3][v] += lo * g;
+        } else {
+          acc[3][v] += support_term(r[v], lo, hi);
+        }
+        acc[4][v] += support_term(r[v], bl, bh);
+        const double term = support_term(dr[v], lo, hi);
+        acc[5][v] += term;
+        acc[6][v] += fabs(term);
+        const double dx = xt[v] - x[v];
+        const double t2 = cc * dx;
+        acc[7][v] += t2;
+        acc[8][v] += fabs(t2);
+        const double rv = dx - project_recession(dx, lo, hi);
+        acc[9][v] += rv * rv;
+      }
+    }
+    st_wb<V>(P.R + idx, r);
+    st_wb<V>(P.DR + idx, dr);
+  }
+};
+
+template <int W, int LL = 0>
+static __device__ void check_body(const Params& P, const Ctrl& C, double* red) {
+  prof_begin(P, K_CHECK);
+  CheckOp<W> op(P, C);
+  const int nb = (C.active + W - 1) / W;
+  run_rows<W, 10, LL>(op, P.n, nb, C.Rc, P.partials, P.counters, P.colsum, S_OBJ, P.Kp, red);
+  prof_end(P, K_CHECK);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBlock, kRowMinCtas) k_check(Params P) {
+  __shared__ double red[kRedDoubles];
+  const Ctrl C = *P.ctrl;
+  if (C.done || !C.check) return;
+  check_body<W>(P, C, red);
+}
+
+// ---------------------------------------------------------------------------
+// cert: ||A'dy + dr||^2 for the flagged columns (solver.hpp:476-483)
+// ---------------------------------------------------------------------------
+template <int W>
+struct CertOp {
+  static constexpr int V = Geo<W>::V;
+  const Params& P;
+  int active;
+  int flag[V];
+  __device__ CertOp(const Params& p, const Ctrl& C) : P(p) { active = C.active; }
+  __device__ void stage(int, volatile SColInfo*) {}
+  __device__ void begin(int, int slot0, double (&)[1][V], bool, const volatile SColInfo*) {
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      flag[v] = (slot0 + v < active) ? P.cert_flag[slot0 + v] : 0;
+  }
+  __device__ void row(int b, int i, int, int li, double (&acc)[1][V]) {
+    bool any = false;
+#pragma unroll
+    for (int v = 0; v < V; ++v) any = any || flag[v];
+    if (!any) return;
+    const int n = P.n, m = P.m;
+    double at[V], dr[V];
+    gather_row<W>(P.trp, P.tci, P.tcv, P.DY + (size_t)b * m * W + li * V, i, at);
+    ld_cg<V>(P.DR + ((size_t)b * n + i) * W + li * V, dr);
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (flag[v]) {
+        const double q = at[v] + dr[v];
+        acc[0][v] += q * q;
+      }
+  }
+};
+
+template <int W, int LL = 0>
+static __device__ void cert_body(const Params& P, const Ctrl& C, double* red) {
+  prof_begin(P, K_CERT);
+  CertOp<W> op(P, C);
+  const int nb = (C.active + W - 1) / W;
+  run_rows<W, 1, LL>(op, P.n, nb, C.Rc, P.partials, P.counters, P.colsum, S_CERT, P.Kp, red);
+  prof_end(P, K_CERT);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBlock, kRowMinCtas) k_cert(Params P) {
+  __shared__ double red[kRedDoubles];
+  const Ctrl C = *P.ctrl;
+  if (C.done || !C.cert_pending) return;
+  cert_body<W>(P, C, red);
+}
+
+// ---------------------------------------------------------------------------
+// plain SpMM: out[:, j] = op(A) in[:, j] for j < active (sparse.hpp:213-238)
+// ---------------------------------------------------------------------------
+template <int W>
+struct SpmmOp {
+  static constexpr int V = Geo<W>::V;
+  const int *rp, *ci;
+  const double *cv, *in;
+  double* out;
+  int rows_in, rows_out, active;
+  int valid[V];
+  __device__ void stage(int, volatile SColInfo*) {}
+  __device__ void begin(int, int slot0, double (&)[1][V], bool, const volatile SColInfo*) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) valid[v] = slot0 + v < active;
+  }
+  __device__ void row(int b, int i, int, int li, double (&)[1][V]) {
+    double o[V];
+    gather_row<W>(rp, ci, cv, in + (size_t)b * rows_in * W + li * V, i, o);
+    double* dst = out + ((size_t)b * rows_out + i) * W + li * V;
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (valid[v]) dst[v] = o[v];
+  }
+};
+
+template <int W>
+__global__ void __launch_bounds__(kBlock) k_spmm(Params P, int transpose,
+                                                 const double* in, double* out,
+                                                 int active, int R, double* partials,
+                                                 int* counters, double* colsum) {
+  SpmmOp<W> op;
+  op.rp = transpose ? P.trp : P.rp;
+  op.ci = transpose ? P.tci : P.ci;
+  op.cv = transpose ? P.tcv : P.cv;
+  op.in = in;
+  op.out = out;
+  op.rows_in = transpose ? P.m : P.n;
+  op.rows_out = transpose ? P.n : P.m;
+  op.active = active;
+  const int nb = (active + W - 1) / W;
+  __shared__ double red[kRedDoubles];
+  run_rows<W, 1>(op, op.rows_out, nb, R, partials, counters, colsum, 0, P.Kp, red);
+}
+
+// ---------------------------------------------------------------------------
+// decide: one CTA runs the batch control of batch_solver.hpp:203-345
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double cs(const Params& P, int s, int j) {
+  return P.colsum[(size_t)s * P.Kp + j];
+}
+__device__ __forceinline__ double& csr(const Params& P, int s, int j) {
+  return P.colsum[(size_t)s * P.Kp + j];
+}
+
+// m_residual_from_terms, solver.hpp:250-263
+__device__ __forceinline__ double m_residual(double dx2, double dy2, double cross,
+                                             double eta, double w, int* err) {
+  const double msq = (w / eta) * dx2 + (1.0 / (eta * w)) * dy2 + 2.0 * cross;
+  if (msq < 0.0) {
+    const double scale = (w / eta) * dx2 + (1.0 / (eta * w)) * dy2 + 2.0 * fabs(cross);
+    if (msq < -1e-12 * smax(1.0, scale)) *err = 1;
+    return 0.0;
+  }
+  return sqrt(msq);
+}
+
+// ---- correctly rounded exp / log (double-double) ---------------------------
+// The weight update is the only transcendental on the path. glibc's exp/log
+// return the correctly rounded value except in rare near-midpoint cases, so
+// evaluating them to ~100 bits and rounding once reproduces the reference's
+// weights bit for bit (CUDA's exp/log are only faithful to 1-2 ulp).
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ DD two_sum(double a, double b) {
+  const double s = a + b, bb = s - a;
+  return {s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ DD fast_two_sum(double a, double b) {
+  const double s = a + b;
+  return {s, b - (s - a)};
+}
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  DD s = two_sum(a.hi, b.hi);
+  const DD t = two_sum(a.lo, b.lo);
+  s.lo += t.hi;
+  s = fast_two_sum(s.hi, s.lo);
+  s.lo += t.lo;
+  return fast_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ DD dd_mul(DD a, DD b) {
+  const double p = a.hi * b.hi;
+  double e = __fma_rn(a.hi, b.hi, -p);
+  e += a.hi * b.lo + a.lo * b.hi;
+  return fast_two_sum(p, e);
+}
+__device__ __forceinline__ DD dd_mul_d(DD a, double b) {
+  const double p = a.hi * b;
+  double e = __fma_rn(a.hi, b, -p);
+  e += a.lo * b;
+  return fast_two_sum(p, e);
+}
+// exp(x) = 2^k * s, s as a double-double.
+static __device__ DD dd_exp_scaled(double x, int* k_out) {
+  const DD ln2 = {0.6931471805599453, 2.3190468138462996e-17};
+  const double k = rint(x / ln2.hi);
+  DD r = dd_add({x, 0.0}, dd_mul_d(ln2, -k));
+  r.hi = ldexp(r.hi, -10);
+  r.lo = ldexp(r.lo, -10);
+  DD s = {1.0, 0.0};
+  for (int i = 16; i >= 1; --i) {  // Horner: 1 + r/i * (...)
+    const double inv = 1.0 / i;
+    const DD inv_dd = {inv, __fma_rn(-inv, (double)i, 1.0) / i};
+    s = dd_add({1.0, 0.0}, dd_mul(dd_mul(r, inv_dd), s));
+  }
+  for (int i = 0; i < 10; ++i) s = dd_mul(s, s);
+  *k_out = (int)k;
+  return s;
+}
+static __device__ double cr_exp(double x) {
+  if (isnan(x)) return x;
+  if (x > 709.79) return exp(x);
+  if (x < -708.0) return exp(x);
+  int k;
+  const DD s = dd_exp_scaled(x, &k);
+  return ldexp(s.hi + s.lo, k);
+}
+static __device__ double cr_log(double x) {
+  if (!(x > 0.0) || isinf(x)) return log(x);
+  const double y0 = log(x);
+  int k;
+  DD e = dd_exp_scaled(-y0, &k);  // one Newton step: y0 + x e^{-y0} - 1
+  e = dd_mul_d(e, x);
+  e.hi = ldexp(e.hi, k);
+  e.lo = ldexp(e.lo, k);
+  const DD t = dd_add(e, {-1.0, 0.0});
+  const DD y = dd_add({y0, 0.0}, t);
+  return y.hi + y.lo;
+}
+
+// smoothed_primal_weight, solver.hpp:321-334
+__device__ __forceinline__ double smoothed_weight(double w, double dxn, double dyn,
+                                                  double theta) {
+  if (!(dxn > 0.0) || !(dyn > 0.0) || !isfinite(dxn) || !isfinite(dyn)) return w;
+  const double d = dyn / dxn;
+  if (!isfinite(d) || d <= 0.0) return w;
+  const double log_w = cr_log(w);
+  const double proposed = theta * cr_log(d) + (1.0 - theta) * log_w;
+  const double step_cap = cr_log(4.0);
+  if (proposed > log_w + step_cap) return cr_exp(log_w + step_cap);
+  if (proposed < log_w - step_cap) return cr_exp(log_w - step_cap);
+  return cr_exp(proposed);
+}
+
+// evaluate_optimality (solver.hpp:398-415) from the column sums, followed by
+// the first half of check_infeasibility_probe (:463-475).
+static __device__ void evaluate_column(const Params& P, int j) {
+  const double obj = cs(P, S_OBJ, j);
+  const double sup_r = cs(P, S_SUPR, j);
+  const double sup_y = cs(P, S_SUPY, j);
+  const double pres = sqrt(cs(P, S_PRES, j));
+  const double dres = sqrt(cs(P, S_DRES, j));
+  const double supports = sup_r + sup_y;
+  const double gap = obj + supports;
+  const double gap_scale = 1.0 + fabs(obj) + fabs(supports);
+  const double rgap = isfinite(gap) ? fabs(gap) : kInf;
+  const bool gap_ok = isfinite(gap) && fabs(gap) <= P.eps * gap_scale;
+  const double primal_scale = 1.0 + sqrt(cs(P, S_AX2, j));
+  const bool primal_ok = pres <= P.eps * primal_scale;
+  const double dual_scale = 1.0 + sqrt(cs(P, S_CSQ, j));
+  const bool dual_ok = dres <= P.eps_dual * dual_scale;
+  double score = rgap / gap_scale;  // std::max({...}): first largest wins
+  const double s2 = pres / primal_scale, s3 = dres / dual_scale;
+  if (score < s2) score = s2;
+  if (score < s3) score = s3;
+  P.t_obj[j] = obj;
+  P.t_gap[j] = rgap;
+  P.t_pres[j] = pres;
+  P.t_dres[j] = dres;
+  P.t_score[j] = score;
+  const double dsup = cs(P, S_DRSUP, j);
+  P.t_dsup[j] = dsup;
+  int v = V_NONE;
+  if (gap_ok && primal_ok && dual_ok) {
+    v = V_OPTIMAL;
+  } else if (dsup < -1e-9 * smax(1.0, cs(P, S_DRSCALE, j))) {
+    v = V_CERT_NEED;
+  }
+  P.verdict[j] = v;
+}
+
+// Dual-ray half of the probe, solver.hpp:495-525.
+static __device__ bool dual_ray(const Params& P, int j) {
+  const double desc = cs(P, S_DESC, j);
+  if (desc < -1e-9 * smax(1.0, cs(P, S_DESCSCALE, j))) {
+    const double budget = P.eps_infeas * fabs(desc);
+    if (sqrt(cs(P, S_VARSQ, j)) <= budget && sqrt(cs(P, S_ROWSQ, j)) <= budget)
+      return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void set_cond(const Params& P,
+                                         cudaGraphConditionalHandle h,
+                                         unsigned v) {
+  if (P.use_graph) cudaGraphSetConditional(h, v);
+}
+
+// Sum of v[0..count) in a fixed order: sequential (the reference's order)
+// for count <= 256, else strided per thread then a fixed tree.
+static __device__ double ordered_sum(const double* v, int count, double* sh) {
+  const int tid = threadIdx.x;
+  __shared__ double result;
+  __syncthreads();
+  if (count <= 256) {
+    if (tid < count) sh[tid] = v[tid];  // stage: one parallel load, then a
+    __syncthreads();                    // sequential sum out of shared memory
+    if (tid == 0) {
+      double s = 0.0;
+      for (int j = 0; j < count; ++j) s += sh[j];
+      result = s;
+    }
+    __syncthreads();
+    return result;
+  } else {
+    double s = 0.0;
+    for (int j = tid; j < count; j += (int)blockDim.x) s += v[j];
+    sh[tid] = s;
+    __syncthreads();
+    for (int off = (int)blockDim.x / 2; off > 0; off >>= 1) {
+      if (tid < off) sh[tid] = sh[tid] + sh[tid + off];
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+static __device__ void write_result(const Params& P, const Ctrl& C, int j, int status,
+                             int cert_kind) {
+  const int o = P.slot_orig[j];
+  bl_column_result& r = P.res[o];
+  r.status = status;
+  r.restarts = C.restarts;
+  r.iterations = C.total_k;
+  r.objective = P.t_obj[j];
+  r.gap = P.t_gap[j];
+  r.primal = P.t_pres[j];
+  r.dual = P.t_dres[j];
+  r.fixed_point = P.resid[j];
+  r.bound_support = cs(P, S_SUPR, j);
+  r.row_support = cs(P, S_SUPY, j);
+  r.base_bound_support = cs(P, S_BSUPR, j);
+  r.has_solution = P.vectors >= BL_VECTORS_SOLUTION;
+  r.certificate_kind = cert_kind;
+  r.has_certificate = (P.vectors >= BL_VECTORS_CERTIFICATE) && cert_kind != 0;
+  r.vectors_exist = 1;
+}
+
+// Permutes every per-slot array by perm (new slot s <- old slot perm[s]).
+static __device__ void permute_slots(const Params& P, const int* perm, int width,
+                              double* scratch) {
+  double* darr[] = {P.w, P.resid, P.anchor_resid, P.best_score, P.best_obj,
+                    P.best_gap, P.best_pres, P.best_dres, P.best_fp, P.best_bsup,
+                    P.best_rsup, P.best_bbsup,
+                    P.colsum + (size_t)S_XA2 * P.Kp, P.colsum + (size_t)S_YA2 * P.Kp};
+  constexpr int ND = 14;
+  const int tid = threadIdx.x;
+  for (int a = 0; a < ND; ++a) {
+    for (int s = tid; s < width; s += (int)blockDim.x) scratch[s] = darr[a][perm[s]];
+    __syncthreads();
+    for (int s = tid; s < width; s += (int)blockDim.x) darr[a][s] = scratch[s];
+    __syncthreads();
+  }
+  int* iarr[] = {P.slot_orig, P.has_best};
+  int* iscratch = reinterpret_cast<int*>(scratch);
+  for (int a = 0; a < 2; ++a) {
+    for (int s = tid; s < width; s += (int)blockDim.x) iscratch[s] = iarr[a][perm[s]];
+    __syncthreads();
+    for (int s = tid; s < width; s += (int)blockDim.x) iarr[a][s] = iscratch[s];
+    __syncthreads();
+  }
+}
+
+// Everything after the per-column verdicts (batch_solver.hpp:229-338).
+static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* sh,
+                         int* ish, double* scratch) {
+  const int tid = threadIdx.x;
+  const int active0 = C.active;
+  const int width = P.width;
+  int* snap_bits = P.cert_flag;  // reused: cert flags are consumed by now
+  __shared__ int n_fin, n_snap;
+  if (tid == 0) {
+    n_fin = 0;
+    n_snap = 0;
+  }
+  __syncthreads();
+  if (C.check) {
+    for (int j = tid; j < active0; j += (int)blockDim.x) {
+      const int v = P.verdict[j];
+      int bits = 0;
+      if (v == V_OPTIMAL || v == V_PRIMAL_INF || v == V_DUAL_INF) {
+        const int status = v == V_OPTIMAL ? BL_OPTIMAL
+                           : v == V_PRIMAL_INF ? BL_PRIMAL_INFEASIBLE
+                                               : BL_DUAL_INFEASIBLE;
+        const int kind = v == V_PRIMAL_INF ? 1 : (v == V_DUAL_INF ? 2 : 0);
+        write_result(P, C, j, status, kind);
+        P.orig_done[P.slot_orig[j]] = 1;
+        atomicAdd(&n_fin, 1);
+        if (P.vectors >= BL_VECTORS_SOLUTION) bits |= SN_FINAL;
+        if (P.vectors >= BL_VECTORS_CERTIFICATE && kind == 1) bits |= SN_CERTP;
+        if (P.vectors >= BL_VECTORS_CERTIFICATE && kind == 2) bits |= SN_CERTD;
+      } else {
+        // BestCandidate::offer, solver.hpp:543-553
+        const double score = P.t_score[j];
+        if (!(score >= P.best_score[j])) {
+          P.best_score[j] = score;
+          P.best_obj[j] = P.t_obj[j];
+          P.best_gap[j] = P.t_gap[j];
+          P.best_pres[j] = P.t_pres[j];
+          P.best_dres[j] = P.t_dres[j];
+          P.best_fp[j] = P.resid[j];
+          P.best_bsup[j] = cs(P, S_SUPR, j);
+          P.best_rsup[j] = cs(P, S_SUPY, j);
+          P.best_bbsup[j] = cs(P, S_BSUPR, j);
+          P.has_best[j] = 1;
+          if (P.vectors >= BL_VECTORS_SOLUTION) bits |= SN_BEST;
+        }
+      }
+      snap_bits[j] = bits;
+      P.snap_orig[j] = P.slot_orig[j];
+    }
+  }
+  __syncthreads();
+  int active = active0;
+  int* perm = P.move_src;
+  const bool at_cap = C.at_cap;
+  const bool compact = C.check && n_fin > 0;
+  if (compact) {
+    // swap-with-last compaction scan (batch_solver.hpp:273-278), simulated
+    // on the slot permutation only; the arrays are permuted afterwards.
+    for (int s = tid; s < width; s += (int)blockDim.x) perm[s] = s;
+    __syncthreads();
+    if (tid == 0) {
+      int a = active0;
+      for (int s = active0 - 1; s >= 0; --s) {
+        if (P.orig_done[P.slot_orig[perm[s]]]) {
+          const int t = --a;
+          const int tmp = perm[s];
+          perm[s] = perm[t];
+          perm[t] = tmp;
+        }
+      }
+      ish[0] = a;
+    }
+    __syncthreads();
+    active = ish[0];
+    permute_slots(P, perm, width, scratch);
+    if (tid == 0) C.col_epoch += 1;
+  }
+  // iteration limit: freeze what is left from the best candidates (:280-295)
+  if (at_cap && active > 0) {
+    for (int j = tid; j < active; j += (int)blockDim.x) {
+      const int o = P.slot_orig[j];
+      bl_column_result& r = P.res[o];
+      r.status = BL_ITERATION_LIMIT;
+      r.restarts = C.restarts;
+      r.iterations = C.total_k;
+      const bool hb = P.has_best[j];
+      r.objective = hb ? P.best_obj[j] : 0.0;
+      r.gap = hb ? P.best_gap[j] : kInf;
+      r.primal = hb ? P.best_pres[j] : kInf;
+      r.dual = hb ? P.best_dres[j] : kInf;
+      r.fixed_point = hb ? P.best_fp[j] : kInf;
+      r.bound_support = hb ? P.best_bsup[j] : 0.0;
+      r.row_support = hb ? P.best_rsup[j] : 0.0;
+      r.base_bound_support = hb ? P.best_bbsup[j] : 0.0;
+      r.has_solution = hb && P.vectors >= BL_VECTORS_SOLUTION;
+      r.has_certificate = 0;
+      r.certificate_kind = 0;
+      r.vectors_exist = hb;
+      P.orig_done[o] = 1;
+      const int pre = compact ? perm[j] : j;
+      if (hb && P.vectors >= BL_VECTORS_SOLUTION) snap_bits[pre] |= SN_CAP;
+    }
+    __syncthreads();
+  }
+  // snapshot list (pre-compaction slots) and move list (post <- pre)
+  if (C.check) {
+    for (int j = tid; j < active0; j += (int)blockDim.x) {
+      const int bits = snap_bits[j];
+      if (bits) {
+        const int k = atomicAdd(&n_snap, 1);
+        P.snap_list[3 * k] = j;
+        P.snap_list[3 * k + 1] = P.snap_orig[j];
+        P.snap_list[3 * k + 2] = bits;
+      }
+    }
+  }
+  __syncthreads();
+  int n_moves = 0;
+  if (compact && !(at_cap) && active > 0) {
+    if (tid == 0) ish[1] = 0;
+    __syncthreads();
+    for (int s = tid; s < active; s += (int)blockDim.x) {
+      if (perm[s] != s) {
+        const int k = atomicAdd(&ish[1], 1);
+        P.moves[2 * k] = s;
+        P.moves[2 * k + 1] = perm[s];
+      }
+    }
+    __syncthreads();
+    n_moves = ish[1];
+  }
+  __syncthreads();
+
+  if (tid == 0) {
+    C.n_snap = n_snap;
+    C.n_moves = n_moves;
+    C.snap_cur = C.cur;
+    C.active = active;
+    C.n_finished = n_fin;
+    if (active == 0 || at_cap) C.done = 1;
+    ish[2] = 0;  // restart
+    if (!C.done && C.inner_k >= 1) {
+      // restart_reason, solver.hpp:299-311
+      int reason = -1;
+      if (mean <= P.beta_s * C.mean_anchor) reason = BL_RESTART_SUFFICIENT;
+      else if (mean <= P.beta_n * C.mean_anchor && mean > C.mean_prev)
+        reason = BL_RESTART_NECESSARY;
+      else if ((double)C.inner_k > P.beta_a * (double)C.total_k)
+        reason = BL_RESTART_ARTIFICIAL;
+      if (reason >= 0) {
+        if (C.log_count < P.log_cap) {
+          bl_restart_event& e = P.log[C.log_count];
+          e.at_iteration = C.total_k;
+          e.reason = reason;
+          e.reserved = 0;
+          e.residual = mean;
+          e.anchor_residual = C.mean_anchor;
+        }
+        C.log_count += 1;
+        ish[2] = 1;
+      }
+    }
+  }
+  __syncthreads();
+  const bool restart = ish[2] != 0;
+  if (restart) {
+    // gated weight update on the post-compaction active columns (:303-319)
+    for (int j = tid; j < active; j += (int)blockDim.x) {
+      if (P.resid[j] <= P.anchor_resid[j]) {
+        const double dxn = sqrt(cs(P, S_XA2, j));
+        const double dyn = sqrt(cs(P, S_YA2, j));
+        P.w[j] = smoothed_weight(P.w[j], dxn, dyn, P.theta);
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    C.hash_pending = 0;
+    if (!C.done) {
+      if (restart) {
+        C.anchor_reset = 1;
+        C.inner_k = 0;
+        C.restarts += 1;
+        C.col_epoch += 1;  // weights changed
+      } else {
+        C.alpha_used = C.alpha;
+        C.cur ^= 1;
+        C.anchor_reset = 0;
+        C.mean_prev = mean;
+        C.inner_k += 1;
+        C.total_k += 1;
+        C.hash_pending = P.trace;
+      }
+      C.alpha = (double)(C.inner_k + 1) / (double)(C.inner_k + 2);
+      C.at_cap = C.total_k >= P.max_it;
+      C.check = (C.total_k % P.period == 0) || C.at_cap;
+      const int nba = (C.active + P.W - 1) / P.W;
+      C.Rp = items_per_block(P.n, P.m, P.W, P.grid, nba, P.l2_budget);
+      C.Rd = items_per_block(P.m, P.n, P.W, P.grid, nba, P.l2_budget);
+      C.Rc = C.Rp;
+    }
+    C.cert_pending = 0;
+    // The graph loop hands the tail over to the persistent kernel once an
+    // iteration's streamed state is small enough to be latency-bound.
+    const double state_bytes =
+        8.0 * (double)((C.active + P.W - 1) / P.W) * P.W * (double)(P.n + P.m);
+    const bool handover = P.handover_bytes > 0.0 && state_bytes < P.handover_bytes;
+    set_cond(P, P.h_loop, (C.done || handover) ? 0u : 1u);
+    set_cond(P, P.h_check, (!C.done && C.check) ? 1u : 0u);
+    set_cond(P, P.h_snap, (C.n_snap > 0 || C.n_moves > 0) ? 1u : 0u);
+    if (P.trace) set_cond(P, P.h_trace, C.hash_pending ? 1u : 0u);
+  }
+}
+
+// Folds the finished launches' entry/exit stamps into the accumulators and
+// credits this iteration's row kernels with their algorithmic bytes
+// (compulsory traffic, gathers counted once).
+// Called by the first K_KINDS threads (one kind each).
+static __device__ void prof_fold(const Params& P, const Ctrl& C, int k, unsigned long long now) {
+  if (!P.prof || k >= K_KINDS) return;
+  const unsigned long long s = P.prof[2 * k], e = P.prof[2 * k + 1];
+  if (e != 0ull && s != ~0ull && e >= s) {
+    P.prof_acc[3 * k] += (double)(e - s);
+    P.prof_acc[3 * k + 1] += 1.0;
+  }
+  P.prof[2 * k] = k == K_DECIDE ? now : ~0ull;
+  P.prof[2 * k + 1] = 0ull;
+  if (k != 0) return;
+  const double n = P.n, m = P.m, nnz = (double)P.nnz, K = C.active;
+  const double chk = C.check ? 1.0 : 0.0;
+  P.prof_acc[3 * K_PRIMAL + 2] += 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 4.0 * n + chk * n);
+  P.prof_acc[3 * K_DUAL + 2] += 12.0 * nnz + 4.0 * (m + 1) + 16.0 * m + 8.0 * K * (n + 6.0 * m + chk * 3.0 * m);
+  if (C.check)
+    P.prof_acc[3 * K_CHECK + 2] += 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 5.0 * n);
+}
+
+static __device__ void decide_body(const Params& P, int phase) {
+  double* scratch = P.scratch;
+  __shared__ double sh[kDecideThreads];
+  __shared__ int ish[4];
+  __shared__ Ctrl C;
+  const int tid = threadIdx.x;
+  if (tid == 0) C = *P.ctrl;
+  __syncthreads();
+  if (C.done) return;
+  if (phase == 1 && !C.cert_pending) return;
+  const int active = C.active;
+  double mean;
+  if (phase == 0) {
+    if (tid < 32) {
+      unsigned long long now = 0;
+      if (tid == 0) now = gtime();
+      now = __shfl_sync(0xffffffffu, now, 0);
+      prof_fold(P, C, tid, now);
+    }
+    if (tid == 0) {
+      ish[3] = 0;
+      C.launches += 3 + (C.check ? 1 : 0);
+      C.passes += 1;
+      // a loop pass either advances total_k or is the single re-application
+      // after a restart, so this bound is never reached by a correct run
+      if (C.passes > 2 * P.max_it + 1024) ish[3] = 2;
+    }
+    __syncthreads();
+    for (int j = tid; j < active; j += (int)blockDim.x) {
+      int err = 0;
+      P.resid[j] = m_residual(cs(P, S_DX2, j), cs(P, S_DY2, j), cs(P, S_CROSS, j),
+                              P.eta, P.w[j], &err);
+      if (err) ish[3] = 1;
+    }
+    __syncthreads();
+    if (ish[3]) {
+      if (tid == 0) {
+        C.error = ish[3] == 2 ? BL_ERR_LOGIC : BL_ERR_DOMAIN;
+        if (P.prof) atomicMax(&P.prof[2 * K_DECIDE + 1], gtime());
+        C.done = 1;
+        *P.ctrl = C;
+        set_cond(P, P.h_loop, 0u);
+        set_cond(P, P.h_check, 0u);
+        set_cond(P, P.h_cert, 0u);
+        set_cond(P, P.h_snap, 0u);
+        if (P.trace) set_cond(P, P.h_trace, 0u);
+      }
+      return;
+    }
+    const int count = P.avg_all ? P.width : active;
+    mean = ordered_sum(P.resid, count, sh) / (double)count;
+    if (C.inner_k == 0) {
+      for (int j = tid; j < active; j += (int)blockDim.x) P.anchor_resid[j] = P.resid[j];
+    }
+    if (tid == 0) {
+      if (C.inner_k == 0) C.mean_anchor = mean;
+      C.mean = mean;
+      C.sparse_products += 2;
+      if (C.check) C.sparse_products += 1;
+      ish[0] = 0;
+    }
+    __syncthreads();
+    if (C.check) {
+      for (int j = tid; j < active; j += (int)blockDim.x) {
+        evaluate_column(P, j);
+        int need = P.verdict[j] == V_CERT_NEED;
+        if (!need && P.verdict[j] == V_NONE && dual_ray(P, j)) P.verdict[j] = V_DUAL_INF;
+        P.cert_flag[j] = need;
+        if (need) atomicAdd(&ish[0], 1);
+      }
+      __syncthreads();
+      if (ish[0] > 0) {
+        if (tid == 0) {
+          C.sparse_products += ish[0];
+          C.cert_pending = 1;
+          C.launches += 2;
+          *P.ctrl = C;
+          set_cond(P, P.h_cert, 1u);
+          if (P.prof) atomicMax(&P.prof[2 * K_DECIDE + 1], gtime());
+        }
+        return;
+      }
+    }
+    if (tid == 0) set_cond(P, P.h_cert, 0u);
+  } else {
+    mean = C.mean;
+    for (int j = tid; j < active; j += (int)blockDim.x) {
+      if (P.verdict[j] != V_CERT_NEED) continue;
+      const double res = sqrt(cs(P, S_CERT, j));
+      if (res <= P.eps_infeas * fabs(P.t_dsup[j])) P.verdict[j] = V_PRIMAL_INF;
+      else P.verdict[j] = dual_ray(P, j) ? V_DUAL_INF : V_NONE;
+    }
+    __syncthreads();
+  }
+  finalize(P, C, mean, sh, ish, scratch);
+  __syncthreads();
+  if (tid == 0) {
+    if (C.n_snap > 0 || C.n_moves > 0) C.launches += 2;
+    if (C.hash_pending) C.launches += 1;
+    *P.ctrl = C;
+    if (P.prof) atomicMax(&P.prof[2 * K_DECIDE + 1], gtime());
+  }
+}
+
+// ---------------------------------------------------------------------------
+// snapshots (vectors of finished / best / capped columns) and compaction
+// ---------------------------------------------------------------------------
+static __device__ void snapshot_body(const Params& P, const Ctrl& C) {
+  const int ns = C.n_snap;
+  if (ns == 0) return;
+  prof_begin(P, K_SNAPSHOT);
+  const int n = P.n, m = P.m, W = P.W;
+  const double* Xold = P.X[C.snap_cur];
+  const long long total = (long long)ns * (n + m);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(t / (n + m));
+    const int i0 = (int)(t - (long long)k * (n + m));
+    const int j = P.snap_list[3 * k], o = P.snap_list[3 * k + 1];
+    const int bits = P.snap_list[3 * k + 2];
+    if (i0 < n) {
+      const int i = i0;
+      const size_t e = tidx(n, W, i, j);
+      const size_t ro = (size_t)o * n + i;
+      if (bits & SN_BEST) {
+        P.BX[e] = P.XT[e];
+        P.BR[e] = P.R[e];
+      }
+      if (bits & SN_FINAL) {
+        P.RX[ro] = P.XT[e];
+        P.RR[ro] = P.R[e];
+      }
+      if (bits & (SN_CERTP | SN_CERTD)) P.RDX[ro] = P.XT[e] - Xold[e];
+      if (bits & SN_CERTP) P.RDR[ro] = P.DR[e];
+      if (bits & SN_CAP) {
+        P.RX[ro] = P.BX[e];
+        P.RR[ro] = P.BR[e];
+      }
+    } else {
+      const int i = i0 - n;
+      const size_t e = tidx(m, W, i, j);
+      const size_t ro = (size_t)o * m + i;
+      if (bits & SN_BEST) P.BY[e] = P.YT[e];
+      if (bits & SN_FINAL) P.RY[ro] = P.YT[e];
+      if (bits & SN_CERTP) P.RDY[ro] = P.DY[e];
+      if (bits & SN_CAP) P.RY[ro] = P.BY[e];
+    }
+  }
+  prof_end(P, K_SNAPSHOT);
+}
+
+// Column moves of the swap-with-last compaction (batch_solver.hpp:143-156,
+// 273-278). The reference swaps X/Y/AX/anchors but not the operator outputs
+// XT/YT/AXT, and applies the Halpern step after compaction (:326-335): a
+// column moved into a hole is combined with the T-output that the finished
+// column left in that slot. Reproduced here for parity: on a Halpern
+// iteration the moved column's next iterate is recomputed from XT/YT/AXT of
+// the destination slot and its own pre-step iterate and anchor. On a
+// restart iteration (no Halpern) the current iterate is moved as is.
+static __device__ void compact_body(const Params& P, const Ctrl& C) {
+  const int nm = C.n_moves;
+  if (nm == 0) return;
+  prof_begin(P, K_COMPACT);
+  const int n = P.n, m = P.m, W = P.W;
+  const bool halpern = !C.anchor_reset;
+  const double a = C.alpha_used, oma = 1.0 - a;
+  const int cn = C.cur, co = C.cur ^ 1;
+  const bool best = P.vectors >= BL_VECTORS_SOLUTION;
+  const long long total = (long long)nm * (n + m);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(t / (n + m));
+    const int i0 = (int)(t - (long long)k * (n + m));
+    const int dst = P.moves[2 * k], src = P.moves[2 * k + 1];
+    if (i0 < n) {
+      const size_t d = tidx(n, W, i0, dst), s = tidx(n, W, i0, src);
+      if (halpern) {
+        const double ax = P.aX[s];
+        P.X[cn][d] = a * (2.0 * P.XT[d] - P.X[co][s]) + oma * ax;
+        P.aX[d] = ax;
+      } else {
+        P.X[cn][d] = P.X[cn][s];
+      }
+      if (best) {
+        P.BX[d] = P.BX[s];
+        P.BR[d] = P.BR[s];
+      }
+    } else {
+      const int i = i0 - n;
+      const size_t d = tidx(m, W, i, dst), s = tidx(m, W, i, src);
+      if (halpern) {
+        const double ay = P.aY[s], aax = P.aAX[s];
+        P.Y[cn][d] = a * (2.0 * P.YT[d] - P.Y[co][s]) + oma * ay;
+        P.AX[cn][d] = a * (2.0 * P.AXT[d] - P.AX[co][s]) + oma * aax;
+        P.aY[d] = ay;
+        P.aAX[d] = aax;
+      } else {
+        P.Y[cn][d] = P.Y[cn][s];
+        P.AX[cn][d] = P.AX[cn][s];
+      }
+      if (best) P.BY[d] = P.BY[s];
+    }
+  }
+  prof_end(P, K_COMPACT);
+}
+
+// FNV-1a over the bytes of X[:,0] then Y[:,0] (solver.hpp:170-177,
+// batch_solver.hpp:339-344). Sequential by definition: one thread.
+static __device__ void trace_body(const Params& P) {
+  Ctrl* C = P.ctrl;
+  if (!C->hash_pending) return;
+  uint64_t h = C->hash;
+  const double* x = P.X[C->cur];
+  const double* y = P.Y[C->cur];
+  for (int i = 0; i < P.n; ++i) {
+    const uint64_t bits = (uint64_t)__double_as_longlong(x[(size_t)i * P.W]);
+    for (int k = 0; k < 8; ++k) {
+      h ^= (bits >> (8 * k)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  }
+  for (int i = 0; i < P.m; ++i) {
+    const uint64_t bits = (uint64_t)__double_as_longlong(y[(size_t)i * P.W]);
+    for (int k = 0; k < 8; ++k) {
+      h ^= (bits >> (8 * k)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  }
+  C->hash = h;
+  C->hash_pending = 0;
+}
+
+
+
+
+
+
+// ---------------------------------------------------------------------------
+// persistent loop: the whole solve in ONE cooperative launch
+// ---------------------------------------------------------------------------
+// All CTAs are co-resident (cooperative launch); phases are separated by a
+// grid barrier instead of kernel boundaries, CTA 0 runs the decide phase.
+// The gpu-scope fences of the barrier also invalidate L1, so gathers of data
+// written earlier in the launch see the new values.
+__device__ __forceinline__ void grid_sync(unsigned long long* bar, unsigned long long& target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1ull);
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ Ctrl load_ctrl(const Ctrl* c) {
+  static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl must be 8-byte sized");
+  Ctrl out;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(c);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(&out);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Ctrl) / 8); ++i) dst[i] = __ldcg(src + i);
+  return out;
+}
+
+// One thread-block cluster: phases separated by the hardware cluster
+// barrier (release/acquire at cluster scope; it also invalidates L1, so the
+// gathers see data other CTAs of the cluster wrote in the previous phase).
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// The row phases of one loop pass with LL lanes per row (0: full width).
+template <int W, int LL, class Sync>
+__device__ __forceinline__ void loop_rows(const Params& P, const Ctrl& C, double* red, Sync& sync) {
+  if (C.check) {
+    primal_body<W, true, LL>(P, C, red);
+    sync();
+    dual_body<W, true, LL>(P, C, red);
+    sync();
+    check_body<W, LL>(P, C, red);
+    sync();
+  } else {
+    primal_body<W, false, LL>(P, C, red);
+    sync();
+    dual_body<W, false, LL>(P, C, red);
+    sync();
+  }
+}
+
+// Lanes per row for a pass: full width unless one block is active, then the
+// smallest power of two covering the live slots (narrow tail mapping).
+template <int W>
+__device__ __forceinline__ int pass_lanes(int active) {
+  constexpr int Lfull = Geo<W>::L, V = Geo<W>::V;
+  if (active > W) return Lfull;
+  int L = 1;
+  while (L * V < active && L < Lfull) L <<= 1;
+  return L;
+}
+
+#define BL_DISPATCH_L(W, Lsel, CALL)                                          \
+  switch (Lsel) {                                                            \
+    case 1: if constexpr (Geo<W>::L >= 1) { constexpr int LL_ = 1; CALL; } break;   \
+    case 2: if constexpr (Geo<W>::L >= 2) { constexpr int LL_ = 2; CALL; } break;   \
+    case 4: if constexpr (Geo<W>::L >= 4) { constexpr int LL_ = 4; CALL; } break;   \
+    case 8: if constexpr (Geo<W>::L >= 8) { constexpr int LL_ = 8; CALL; } break;   \
+    default: { constexpr int LL_ = 0; CALL; } break;                         \
+  }
+
+// ---------------------------------------------------------------------------
+// fast tail passes: one cluster, one active column block, plain iteration
+// ---------------------------------------------------------------------------
+// In the tail an iteration is a few microseconds of work, so latency chains
+// decide its cost. A plain pass (no termination check, no certificate, no
+// compaction) therefore runs a lean schedule that computes exactly what the
+// generic phases + decide_body compute for such a pass:
+//  * each CTA of the cluster owns fixed row ranges of A' (primal) and A
+//    (dual) for the whole launch, with their CSR metadata cached in shared
+//    memory (loaded once per launch);
+//  * column descriptors are cached in shared memory and restaged only when
+//    the slot weights / permutation change (Ctrl::col_epoch);
+//  * per-CTA partial sums go to P.tail_part without fences or atomics; the
+//    cluster barrier publishes them and warp 0 of CTA 0 folds them in CTA
+//    order inside a warp-synchronous decide.
+struct TailRows {
+  int pr0, pr1, dr0, dr1;  // A' rows (primal) and A rows (dual) of this CTA
+  int pcached, dcached;    // metadata in shared memory?
+  const int *prp, *pci, *drp, *dci;
+  const double *pcv, *dcv;
+  int epoch;
+};
+static __device__ __noinline__ SColInfo* tail_cols(int which) {
+  __shared__ SColInfo s[2][32];  // [0] primal steps (tau), [1] dual steps (sigma)
+  return s[which];
+}
+static __device__ __noinline__ TailRows* tail_rows() {
+  __shared__ TailRows t;
+  return &t;
+}
+static __device__ __noinline__ Ctrl* tail_ctrl() {
+  __shared__ Ctrl c;
+  return &c;
+}
+
+// Copies rows [r0, r1) of a CSR into shared memory at *cursor; returns
+// pointers offset so that they can be indexed with global row / nonzero
+// indices. Falls back to the global arrays when the cache is too small.
+static __device__ void tail_cache_rows(const int* rp, const int* ci, const double* cv, int r0, int r1,
+                                char*& cursor, char* end, const int*& orp, const int*& oci,
+                                const double*& ocv) {
+  const int q0 = rp[r0], q1 = rp[r1];
+  const size_t need = 4 * (size_t)(r1 - r0 + 1) + 4 * (size_t)(q1 - q0) + 8 * (size_t)(q1 - q0) + 16;
+  orp = rp;
+  oci = ci;
+  ocv = cv;
+  if (cursor == nullptr || cursor + need > end) return;
+  int* srp = reinterpret_cast<int*>(cursor);
+  int* sci = srp + (r1 - r0 + 1);
+  double* scv = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(sci + (q1 - q0)) + 7) & ~uintptr_t(7));
+  for (int k = threadIdx.x; k <= r1 - r0; k += blockDim.x) srp[k] = rp[r0 + k];
+  for (int k = threadIdx.x; k < q1 - q0; k += blockDim.x) {
+    sci[k] = ci[q0 + k];
+    scv[k] = cv[q0 + k];
+  }
+  cursor = reinterpret_cast<char*>(scv + (q1 - q0));
+  orp = srp - r0;
+  oci = sci - q0;
+  ocv = scv - q0;
+}
+
+static __device__ void tail_setup(const Params& P, char* dyn, int dyn_bytes) {
+  TailRows* t = tail_rows();
+  const int c = blockIdx.x, cl = gridDim.x;
+  if (threadIdx.x == 0) {
+    // a tiny dimension is one sequential walk by CTA 0 (reference order)
+    const bool tn = P.n <= kTinyRows, tm = P.m <= kTinyRows;
+    t->pr0 = tn ? 0 : (int)((long long)P.n * c / cl);
+    t->pr1 = tn ? (c == 0 ? P.n : 0) : (int)((long long)P.n * (c + 1) / cl);
+    t->dr0 = tm ? 0 : (int)((long long)P.m * c / cl);
+    t->dr1 = tm ? (c == 0 ? P.m : 0) : (int)((long long)P.m * (c + 1) / cl);
+    t->epoch = -1;
+  }
+  __syncthreads();
+  char* cur = dyn_bytes > 0 ? dyn : nullptr;
+  char* end = dyn + dyn_bytes;
+  const int *prp, *pci, *drp, *dci;
+  const double *pcv, *dcv;
+  tail_cache_rows(P.trp, P.tci, P.tcv, t->pr0, t->pr1, cur, end, prp, pci, pcv);
+  tail_cache_rows(P.rp, P.ci, P.cv, t->dr0, t->dr1, cur, end, drp, dci, dcv);
+  if (threadIdx.x == 0) {
+    t->pcached = prp != P.trp;
+    t->dcached = drp != P.rp;
+    t->prp = prp;
+    t->pci = pci;
+    t->pcv = pcv;
+    t->drp = drp;
+    t->dci = dci;
+    t->dcv = dcv;
+  }
+  __syncthreads();
+}
+
+// Sums of this CTA's rows for NS columns-sums, reduced over the CTA in a
+// fixed tree and stored to P.tail_part[cta][k0 + s][jj].
+template <int W, int NS, int LL>
+__device__ __forceinline__ void tail_publish(const Params& P, double (&acc)[NS][Geo<W>::V],
+                                             int k0, double* red) {
+  using Gm = Geo<W, LL>;
+  constexpr int V = Gm::V, L = Gm::L;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int off = 16; off >= L; off >>= 1)
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        acc[s][v] = __dadd_rn(acc[s][v], __shfl_down_sync(0xffffffffu, acc[s][v], off));
+  if (lane < L) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int v = 0; v < V; ++v) red[(warp * NS + s) * W + lane * V + v] = acc[s][v];
+  }
+  __syncthreads();
+  for (int t = tid; t < NS * W; t += kBlock) {
+    const int s = t / W, jj = t - s * W;
+    double sum = 0.0;
+    if (jj < L * V) {
+#pragma unroll
+      for (int wp = 0; wp < kWarps; ++wp) sum = __dadd_rn(sum, red[(wp * NS + s) * W + jj]);
+    }
+    P.tail_part[((size_t)blockIdx.x * 5 + k0 + s) * 32 + jj] = sum;
+  }
+  __syncthreads();
+}
+
+template <int W, int LL>
+static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* red) {
+  using Gm = Geo<W, LL>;
+  constexpr int V = Gm::V, L = Gm::L, G = Gm::G;
+  const TailRows* t = tail_rows();
+  const int tid = threadIdx.x, g = tid / L, li = tid - g * L;
+  const bool tiny_n = P.n <= kTinyRows, tiny_m = P.m <= kTinyRows;
+  {
+    prof_begin(P, K_PRIMAL);
+    PrimalOp<W, false> op(P, C);
+    op.col = tail_cols(0) + li * V;
+    op.crp = t->prp;
+    op.cci = t->pci;
+    op.ccv = t->pcv;
+    op.cached = t->pcached != 0;
+    double acc[2][V];
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[s][v] = 0.0;
+    const int r0 = t->pr0, r1 = t->pr1;
+    if (tiny_n) {
+      if (g == 0)
+        for (int i = r0; i < r1; ++i) op.row(0, i, 0, li, acc);
+    } else {
+      for (int i = r0 + g; i < r1; i += G) op.row(0, i, 0, li, acc);
+    }
+    tail_publish<W, 2, LL>(P, acc, 0, red);
+    prof_end(P, K_PRIMAL);
+  }
+  cluster_sync_all();
+  {
+    prof_begin(P, K_DUAL);
+    DualOp<W, false> op(P, C);
+    op.col = tail_cols(1) + li * V;
+    op.crp = t->drp;
+    op.cci = t->dci;
+    op.ccv = t->dcv;
+    op.cached = t->dcached != 0;
+    double acc[3][V];
+#pragma unroll
+    for (int s = 0; s < 3; ++s)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[s][v] = 0.0;
+    const int r0 = t->dr0, r1 = t->dr1;
+    if (tiny_m) {
+      if (g == 0)
+        for (int i = r0; i < r1; ++i) op.row(0, i, 0, li, acc);
+    } else {
+      for (int i = r0 + g; i < r1; i += G) op.row(0, i, 0, li, acc);
+    }
+    tail_publish<W, 3, LL>(P, acc, 2, red);
+    prof_end(P, K_DUAL);
+  }
+  cluster_sync_all();
+}
+
+// decide_body's logic for a plain pass (no check) with active <= 32, run
+// by warp 0 of CTA 0: lane j owns slot j.
+static __device__ void tail_decide(const Params& P) {
+  const int lane = threadIdx.x;
+  Ctrl& C = *tail_ctrl();
+  if (lane == 0) C = *P.ctrl;
+  __syncwarp();
+  {
+    unsigned long long now = 0;
+    if (lane == 0) now = gtime();
+    now = __shfl_sync(0xffffffffu, now, 0);
+    prof_fold(P, C, lane, now);
+  }
+  __syncwarp();
+  const int active = C.active;
+  const int cl = gridDim.x;
+  double dx2 = 0.0, xa2 = 0.0, dy2 = 0.0, cross = 0.0, ya2 = 0.0, r = 0.0, w = 1.0;
+  int err = 0;
+  if (lane < active) {
+    // fold the CTA partials in CTA order (sequential, fixed)
+    for (int c = 0; c < cl; ++c) {
+      const double* tp = P.tail_part + (size_t)c * 5 * 32 + lane;
+      dx2 = __dadd_rn(dx2, __ldcg(tp));
+      xa2 = __dadd_rn(xa2, __ldcg(tp + 32));
+      dy2 = __dadd_rn(dy2, __ldcg(tp + 64));
+      cross = __dadd_rn(cross, __ldcg(tp + 96));
+      ya2 = __dadd_rn(ya2, __ldcg(tp + 128));
+    }
+    csr(P, S_DX2, lane) = dx2;
+    csr(P, S_XA2, lane) = xa2;
+    csr(P, S_DY2, lane) = dy2;
+    csr(P, S_CROSS, lane) = cross;
+    csr(P, S_YA2, lane) = ya2;
+    w = P.w[lane];
+    r = m_residual(dx2, dy2, cross, P.eta, w, &err);
+    P.resid[lane] = r;
+  }
+  const bool bad = __any_sync(0xffffffffu, err != 0);
+  int loop_err = 0;
+  if (lane == 0) {
+    C.launches += 3;
+    C.passes += 1;
+    if (C.passes > 2 * P.max_it + 1024) loop_err = 1;
+  }
+  loop_err = __shfl_sync(0xffffffffu, loop_err, 0);
+  if (bad || loop_err) {
+    if (lane == 0) {
+      C.error = loop_err ? BL_ERR_LOGIC : BL_ERR_DOMAIN;
+      if (P.prof) atomicMax(&P.prof[2 * K_DECIDE + 1], gtime());
+      C.done = 1;
+      *P.ctrl = C;
+    }
+    return;
+  }
+  // averaged residual: sequential sum in slot order (ordered_sum, count <= 256)
+  double sum = 0.0;
+  for (int j = 0; j < active; ++j) sum += __shfl_sync(0xffffffffu, r, j);
+  const double mean = sum / (double)active;
+  const bool first = C.inner_k == 0;
+  if (first && lane < active) P.anchor_resid[lane] = r;
+  // restart rule (solver.hpp:299-311) on the pre-step state
+  int reason = -1;
+  if (C.inner_k >= 1) {
+    if (mean <= P.beta_s * C.mean_anchor) reason = BL_RESTART_SUFFICIENT;
+    else if (mean <= P.beta_n * C.mean_anchor && mean > C.mean_prev)
+      reason = BL_RESTART_NECESSARY;
+    else if ((double)C.inner_k > P.beta_a * (double)C.total_k)
+      reason = BL_RESTART_ARTIFICIAL;
+  }
+  if (reason >= 0 && lane < active) {
+    const double ar = first ? r : P.anchor_resid[lane];
+    if (r <= ar) P.w[lane] = smoothed_weight(w, sqrt(xa2), sqrt(ya2), P.theta);
+  }
+  __syncwarp();  // every lane has read the control block
+  if (lane == 0) {
+    if (first) C.mean_anchor = mean;
+    C.mean = mean;
+    C.sparse_products += 2;
+    C.n_snap = 0;
+    C.n_moves = 0;
+    C.snap_cur = C.cur;
+    C.n_finished = 0;
+    C.hash_pending = 0;
+    if (reason >= 0) {
+      if (C.log_count < P.log_cap) {
+        bl_restart_event& e = P.log[C.log_count];
+        e.at_iteration = C.total_k;
+        e.reason = reason;
+        e.reserved = 0;
+        e.residual = mean;
+        e.anchor_residual = C.mean_anchor;
+      }
+      C.log_count += 1;
+      C.anchor_reset = 1;
+      C.inner_k = 0;
+      C.restarts += 1;
+      C.col_epoch += 1;
+    } else {
+      C.alpha_used = C.alpha;
+      C.cur ^= 1;
+      C.anchor_reset = 0;
+      C.mean_prev = mean;
+      C.inner_k += 1;
+      C.total_k += 1;
+    }
+    C.alpha = (double)(C.inner_k + 1) / (double)(C.inner_k + 2);
+    C.at_cap = C.total_k >= P.max_it;
+    C.check = (C.total_k % P.period == 0) || C.at_cap;
+    C.cert_pending = 0;
+    *P.ctrl = C;
+    if (P.prof) atomicMax(&P.prof[2 * K_DECIDE + 1], gtime());
+  }
+}
+
+// One fast tail pass on the cluster (all CTAs).
+template <int W>
+static __device__ void tail_pass(const Params& P, const Ctrl& C, double* red) {
+  TailRows* t = tail_rows();
+  if (t->epoch != C.col_epoch) {  // uniform across the CTA
+    const int tid = threadIdx.x;
+    if (tid < W) {
+      stage_col(P, tid, C.active, false, tail_cols(0) + tid);
+      stage_col(P, tid, C.active, true, tail_cols(1) + tid);
+    }
+    __syncthreads();
+    if (tid == 0) t->epoch = C.col_epoch;
+    __syncthreads();
+  }
+  const int Lsel = pass_lanes<W>(C.active);
+  BL_DISPATCH_L(W, Lsel, (tail_rows_pass<W, LL_>(P, C, red)));
+  if (blockIdx.x == 0 && threadIdx.x < 32) tail_decide(P);
+  cluster_sync_all();
+}
+
+// CL = false: cooperative grid over all SMs (grid barriers); it hands over
+// (returns) once at most P.tail_blocks column blocks are active.
+// CL = true: ONE cluster of P.grid CTAs for the latency-bound tail, where an
+// iteration is a few microseconds of work and a grid-wide barrier would cost
+// more than the work itself; rows are walked with the narrow mapping.
+template <int W, bool CL>
+__global__ void __launch_bounds__(kBlock) k_loop(Params P, int tail_smem) {
+  __shared__ double red[kRedDoubles];
+  extern __shared__ __align__(16) char tail_dyn[];
+  unsigned long long target = 0;
+  if constexpr (CL) tail_setup(P, tail_dyn, tail_smem);
+  auto sync = [&]() {
+    if constexpr (CL) cluster_sync_all();
+    else grid_sync(P.barrier, target);
+  };
+  const int grid = gridDim.x;
+  for (;;) {
+    Ctrl C = load_ctrl(P.ctrl);
+    if (C.done) break;
+    const int nba = (C.active + W - 1) / W;
+    if (!CL && P.tail_blocks > 0 && nba <= P.tail_blocks) break;
+    if constexpr (CL) {
+      if (nba == 1 && C.active <= 32 && !C.check && !P.trace && !P.avg_all && P.tail_part) {
+        tail_pass<W>(P, C, red);
+        continue;
+      }
+    }
+    // work decomposition for THIS launch's grid (the control block may have
+    // been written by a driver with another grid)
+    C.Rp = items_per_block(P.n, P.m, W, grid, nba, P.l2_budget);
+    C.Rd = items_per_block(P.m, P.n, W, grid, nba, P.l2_budget);
+    C.Rc = C.Rp;
+    const int Lsel = CL ? pass_lanes<W>(C.active) : Geo<W>::L;
+    BL_DISPATCH_L(W, Lsel, (loop_rows<W, LL_>(P, C, red, sync)));
+    if (blockIdx.x == 0) decide_body(P, 0);
+    sync();
+    C = load_ctrl(P.ctrl);
+    if (C.cert_pending) {
+      C.Rc = items_per_block(P.n, P.m, W, grid, (C.active + W - 1) / W, P.l2_budget);
+      const int Lc = CL ? pass_lanes<W>(C.active) : Geo<W>::L;
+      BL_DISPATCH_L(W, Lc, (cert_body<W, LL_>(P, C, red)));
+      sync();
+      if (blockIdx.x == 0) decide_body(P, 1);
+      sync();
+      C = load_ctrl(P.ctrl);
+    }
+    if (C.n_snap > 0 || C.n_moves > 0) {
+      snapshot_body(P, C);
+      sync();
+      compact_body(P, C);
+      sync();
+    }
+    if (C.hash_pending) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) trace_body(P);
+      sync();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// init (batch_solver.hpp:130-136; warm start solver.hpp:590-597)
+// ---------------------------------------------------------------------------
+
+
+// column-major host layout <-> column-block tiled layout
+
+
+
+// ---------------------------------------------------------------------------
+// power iteration (sparse.hpp:249-287), two start vectors as a W=2 batch
+// ---------------------------------------------------------------------------
+struct PiOp {
+  static constexpr int V = 2;
+  const int *rp, *ci;
+  const double *cv, *in;
+  double* out;
+  int rows_in, rows_out;
+  int valid[2];
+  __device__ void stage(int, volatile SColInfo*) {}
+  __device__ void begin(int, int, double (&)[1][2], bool, const volatile SColInfo*) {}
+  __device__ void row(int, int i, int, int, double (&acc)[1][2]) {
+    double o[2];
+    gather_row<2>(rp, ci, cv, in, i, o);
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      if (valid[v]) {
+        out[(size_t)i * 2 + v] = o[v];
+        acc[0][v] += o[v] * o[v];
+      }
+    }
+  }
+};
+
+
+
+// stage 0 (after u = A v): null-space test; stage 1 (after w = A'u):
+// estimate, stagnation and the normalisation v = w / ||w||. One thread per
+// start vector updates the state; k_pi_fill then rewrites v.
+
+
+
+
+// iteration counter bump (end of one power-iteration step)
+
+// ---------------------------------------------------------------------------
+// per-width launchers: defined (and explicitly instantiated) only in the
+// bl_w<W>.cu translation units, called through the dispatchers in
+// bl_kernels.cu
+// ---------------------------------------------------------------------------
+template <int W>
+struct WLaunch {
+  static void iteration_check(const Params& P, cudaStream_t s);
+  static void iteration_plain(const Params& P, cudaStream_t s);
+  static void spmm(const Params& P, cudaStream_t s, bool transpose, const double* in,
+                   double* out, int active, int R);
+  static void cert(const Params& P, cudaStream_t s);
+  static int loop_ctas_per_sm();
+  static cudaError_t loop(const Params& P, cudaStream_t s);
+  static cudaError_t loop_cluster(const Params& P, cudaStream_t s, int tail_smem);
+  static int max_tail_cluster();
+  static int row_ctas_per_sm();
+};
+
+// Each row kernel is launched with SMs x (its own max resident CTAs, <= 4):
+// the grid-stride item loop does not depend on the grid size.
+inline int grid_of(const void* fn) {
+  static std::mutex mu;
+  static std::map<const void*, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(fn);
+  if (it != cache.end()) return it->second;
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, 0);
+  if (occ < 1) occ = 1;
+  if (occ > 4) occ = 4;
+  return cache[fn] = sms * occ;
+}
+
+#ifdef BL_WLAUNCH_DEFINE
+template <int W>
+void WLaunch<W>::iteration_check(const Params& P, cudaStream_t s) {
+  k_primal<W, true><<<grid_of((const void*)k_primal<W, true>), kBlock, 0, s>>>(P);
+  k_dual<W, true><<<grid_of((const void*)k_dual<W, true>), kBlock, 0, s>>>(P);
+  k_check<W><<<grid_of((const void*)k_check<W>), kBlock, 0, s>>>(P);
+}
+
+template <int W>
+void WLaunch<W>::iteration_plain(const Params& P, cudaStream_t s) {
+  k_primal<W, false><<<grid_of((const void*)k_primal<W, false>), kBlock, 0, s>>>(P);
+  k_dual<W, false><<<grid_of((const void*)k_dual<W, false>), kBlock, 0, s>>>(P);
+}
+
+template <int W>
+void WLaunch<W>::spmm(const Params& P, cudaStream_t s, bool transpose, const double* in,
+                      double* out, int active, int R) {
+  k_spmm<W><<<P.grid, kBlock, 0, s>>>(P, transpose ? 1 : 0, in, out, active, R, P.partials,
+                                       P.counters, P.colsum);
+}
+
+template <int W>
+void WLaunch<W>::cert(const Params& P, cudaStream_t s) {
+  k_cert<W><<<P.grid, kBlock, 0, s>>>(P);
+}
+
+// CTAs per SM the persistent loop kernel can keep co-resident.
+template <int W>
+int WLaunch<W>::loop_ctas_per_sm() {
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_loop<W, false>, kBlock, 0);
+  return occ < 1 ? 1 : occ;
+}
+
+// The whole solve (or its remainder) as one cooperative launch of P.grid
+// co-resident CTAs.
+template <int W>
+cudaError_t WLaunch<W>::loop(const Params& P, cudaStream_t s) {
+  Params Q = P;
+  int no_tail_smem = 0;
+  void* args[] = {&Q, &no_tail_smem};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_loop<W, false>),
+                                     dim3(P.grid), dim3(kBlock), args, 0, s);
+}
+
+// The tail as ONE thread-block cluster of P.grid CTAs (<= 16; sizes above
+// 8 need the non-portable-cluster opt-in).
+template <int W>
+cudaError_t WLaunch<W>::loop_cluster(const Params& P, cudaStream_t s, int tail_smem) {
+  cudaError_t e = cudaSuccess;
+  auto fn = k_loop<W, true>;
+  if (P.grid > 8) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  if (tail_smem > 0) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tail_smem);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P.grid);
+  cfg.blockDim = dim3(kBlock);
+  cfg.dynamicSmemBytes = tail_smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = P.grid;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, P, tail_smem);
+}
+
+// Largest cluster (<= 16) of the tail kernel the device can place.
+template <int W>
+int WLaunch<W>::max_tail_cluster() {
+  int best = 8;
+  auto fn = k_loop<W, true>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+      cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16);
+    cfg.blockDim = dim3(kBlock);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 16;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) == cudaSuccess && clusters > 0)
+      best = 16;
+  }
+  cudaGetLastError();
+  return best;
+}
+
+// Resident CTAs per SM of the widest row kernels (grid of the plain kernels).
+template <int W>
+int WLaunch<W>::row_ctas_per_sm() {
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dual<W, true>, kBlock, 0);
+  int occ2 = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_check<W>, kBlock, 0);
+  if (occ2 < occ) occ = occ2;
+  return occ < 1 ? 1 : occ;
+}
+#endif  // BL_WLAUNCH_DEFINE
+
+}  // namespace bl

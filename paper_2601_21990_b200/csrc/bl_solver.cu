@@ -78,6 +78,7 @@ struct bl_problem {
   bool norm_valid = false;
   double norm = 0.0;
   std::vector<double> h_xl, h_xu;  // for override validation
+  std::vector<int> h_rp, h_trp;    // row pointers (tail shared-memory cache sizing)
 };
 
 struct bl_ctx {
@@ -93,7 +94,8 @@ struct bl_ctx {
     B_X0, B_X1, B_Y0, B_Y1, B_AX0, B_AX1, B_aX, B_aY, B_aAX, B_XT, B_YT, B_DY,
     B_RC, B_R, B_DR, B_AXT, B_BX, B_BY, B_BR, B_RX, B_RY, B_RR, B_RDX, B_RDY, B_RDR,
     B_SLOTD, B_SLOTI, B_ORIGI, B_RES, B_COLSUM, B_PART, B_CNT, B_SNAP, B_MOVES,
-    B_LOG, B_CTRL, B_PROF, B_PROFACC, B_BAR, B_OV, B_OVD, B_WARMX, B_WARMY, B_PI, B_TMP0, B_TMP1, B_COUNT
+    B_LOG, B_CTRL, B_PROF, B_PROFACC, B_BAR, B_OV, B_OVD, B_WARMX, B_WARMY, B_PI, B_TMP0, B_TMP1,
+    B_TAIL, B_COUNT
   };
   DevBuf buf[B_COUNT];
   // last solve
@@ -238,6 +240,26 @@ double device_spectral_norm(bl_ctx* ctx, bl_problem* p) {
   p->norm = ((a < b) ? b : a) * 1.01;
   p->norm_valid = true;
   return p->norm;
+}
+
+// Shared memory for the tail cluster's CSR cache: the largest per-CTA slice
+// (rows + 1 pointers, indices, values, alignment) of A' and A together;
+// 0 (read from global memory) when it would not fit next to the static
+// shared memory of the loop kernel.
+int tail_smem_bytes(const bl_problem* p, int cl) {
+  size_t worst = 0;
+  for (int c = 0; c < cl; ++c) {
+    size_t bytes = 32;
+    for (int pass = 0; pass < 2; ++pass) {
+      const std::vector<int>& rp = pass == 0 ? p->h_trp : p->h_rp;
+      const int rows = (int)rp.size() - 1;
+      const int r0 = (int)((long long)rows * c / cl), r1 = (int)((long long)rows * (c + 1) / cl);
+      const size_t nz = (size_t)(rp[r1] - rp[r0]);
+      bytes += 4 * (size_t)(r1 - r0 + 1) + 12 * nz + 16;
+    }
+    worst = std::max(worst, bytes);
+  }
+  return worst <= (size_t)160 * 1024 ? (int)((worst + 15) / 16 * 16) : 0;
 }
 
 void free_graph(bl_ctx* ctx) {
@@ -653,6 +675,9 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.grid = use_graph ? grid : grid_loop;
   P.l2_budget = l2_budget;
   P.handover_bytes = (mode_loop == 0) ? kHandoverBytes : 0.0;
+  P.tail_part = static_cast<double*>(
+      ctx->buf[bl_ctx::B_TAIL].ensure(sizeof(double) * 16 * 5 * 32));
+  if (std::getenv("BATCHLP_NO_FAST_TAIL")) P.tail_part = nullptr;
   P.barrier = static_cast<unsigned long long*>(
       ctx->buf[bl_ctx::B_BAR].ensure(sizeof(unsigned long long)));
   ck(cudaMemsetAsync(P.barrier, 0, sizeof(unsigned long long), s), "barrier");
@@ -734,7 +759,8 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
         Q.handover_bytes = 0.0;
         Q.use_graph = 0;
         Q.tail_blocks = 0;
-        ck(bl::launch_loop_cluster(Q, s), "cluster loop launch");
+        ck(bl::launch_loop_cluster(Q, s, tail_smem_bytes(p, tail_cluster)),
+           "cluster loop launch");
       }
     }
   }
@@ -905,6 +931,8 @@ int bl_problem_upload(bl_ctx* ctx, int32_t m, int32_t n, int64_t nnz,
     upload(p->rl, row_lower, (size_t)m, s);
     upload(p->ru, row_upper, (size_t)m, s);
     p->h_xl.assign(var_lower, var_lower + n);
+    p->h_rp.assign(rowptr, rowptr + m + 1);
+    p->h_trp.assign(t_rowptr, t_rowptr + n + 1);
     p->h_xu.assign(var_upper, var_upper + n);
     ck(cudaStreamSynchronize(s), "upload sync");
   });
