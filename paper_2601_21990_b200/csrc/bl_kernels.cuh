@@ -265,6 +265,15 @@ static __device__ __noinline__ SColInfo* col_smem() {
 #define BL_ROW_MIN_CTAS 3
 #endif
 constexpr int kRowMinCtas = BL_ROW_MIN_CTAS;
+// the primal kernel carries fewer per-row sums and fits 4 CTAs per SM
+#ifndef BL_PRIMAL_MIN_CTAS
+#define BL_PRIMAL_MIN_CTAS 4
+#endif
+constexpr int kPrimalMinCtas = BL_PRIMAL_MIN_CTAS;
+#ifndef BL_DUAL_MIN_CTAS
+#define BL_DUAL_MIN_CTAS 4
+#endif
+constexpr int kDualMinCtas = BL_DUAL_MIN_CTAS;
 
 // Walks the work items of a persistent row kernel. Op provides:
 //   begin(b, slot0, acc, owner)  per item (owner: holds the matrix's row 0)
@@ -467,7 +476,7 @@ static __device__ void primal_body(const Params& P, const Ctrl& C, double* red) 
 }
 
 template <int W, bool CHECK>
-__global__ void __launch_bounds__(kBlock, kRowMinCtas) k_primal(Params P) {
+__global__ void __launch_bounds__(kBlock, kPrimalMinCtas) k_primal(Params P) {
   __shared__ double red[kRedDoubles];
   const Ctrl C = *P.ctrl;
   if (C.done) return;
@@ -586,7 +595,7 @@ static __device__ void dual_body(const Params& P, const Ctrl& C, double* red) {
 }
 
 template <int W, bool CHECK>
-__global__ void __launch_bounds__(kBlock, kRowMinCtas) k_dual(Params P) {
+__global__ void __launch_bounds__(kBlock, kDualMinCtas) k_dual(Params P) {
   __shared__ double red[kRedDoubles];
   const Ctrl C = *P.ctrl;
   if (C.done) return;
@@ -1083,20 +1092,47 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
   if (compact) {
     // swap-with-last compaction scan (batch_solver.hpp:273-278), simulated
     // on the slot permutation only; the arrays are permuted afterwards.
-    for (int s = tid; s < width; s += (int)blockDim.x) perm[s] = s;
+    // The scan visits s = active0-1 .. 0 and swaps a finished slot with the
+    // current end. A position is never modified before it is visited (swap
+    // partners lie above it), so its "finished" flag is the static one:
+    // the flags are gathered in parallel into a bitmask and one thread walks
+    // only the set bits, with the permutation in shared memory when it fits.
+    unsigned* fw = reinterpret_cast<unsigned*>(sh);        // flag words
+    const int nwords = (active0 + 31) / 32;
+    const bool perm_smem = nwords + active0 <= kDecideScratchInts;
+    int* sp = perm_smem ? reinterpret_cast<int*>(sh) + nwords : perm;
+    for (int s = tid; s < width; s += (int)blockDim.x) {
+      perm[s] = s;
+      if (perm_smem && s < active0) sp[s] = s;
+    }
+    for (int w = tid; w < nwords; w += (int)blockDim.x) {
+      unsigned bits = 0u;
+      for (int b = 0; b < 32; ++b) {
+        const int s = 32 * w + b;
+        if (s < active0 && P.orig_done[P.slot_orig[s]]) bits |= 1u << b;
+      }
+      fw[w] = bits;
+    }
     __syncthreads();
     if (tid == 0) {
       int a = active0;
-      for (int s = active0 - 1; s >= 0; --s) {
-        if (P.orig_done[P.slot_orig[perm[s]]]) {
+      for (int w = nwords - 1; w >= 0; --w) {
+        unsigned bits = fw[w];
+        while (bits) {
+          const int b = 31 - __clz(bits);
+          bits &= ~(1u << b);
+          const int s = 32 * w + b;
           const int t = --a;
-          const int tmp = perm[s];
-          perm[s] = perm[t];
-          perm[t] = tmp;
+          const int tmp = sp[s];
+          sp[s] = sp[t];
+          sp[t] = tmp;
         }
       }
       ish[0] = a;
     }
+    __syncthreads();
+    if (perm_smem)
+      for (int s = tid; s < active0; s += (int)blockDim.x) perm[s] = sp[s];
     __syncthreads();
     active = ish[0];
     permute_slots(P, perm, width, scratch);
@@ -1263,7 +1299,7 @@ static __device__ void prof_fold(const Params& P, const Ctrl& C, int k, unsigned
 
 static __device__ void decide_body(const Params& P, int phase) {
   double* scratch = P.scratch;
-  __shared__ double sh[kDecideThreads];
+  __shared__ double sh[kDecideScratchInts / 2];
   __shared__ int ish[4];
   __shared__ Ctrl C;
   const int tid = threadIdx.x;
