@@ -2074,6 +2074,12 @@ inline int grid_of(const void* fn) {
 }
 
 #ifdef BL_WLAUNCH_DEFINE
+}  // namespace bl
+#ifdef BL_WITH_TMA
+#include "bl_tma.cuh"
+#endif
+namespace bl {
+
 template <int W>
 void WLaunch<W>::iteration_check(const Params& P, cudaStream_t s) {
   k_primal<W, true><<<grid_of((const void*)k_primal<W, true>), kBlock, 0, s>>>(P);
@@ -2083,6 +2089,26 @@ void WLaunch<W>::iteration_check(const Params& P, cudaStream_t s) {
 
 template <int W>
 void WLaunch<W>::iteration_plain(const Params& P, cudaStream_t s) {
+#ifdef BL_WITH_TMA
+  if constexpr (W == 32) {
+    if (P.tma_host) {  // TMA-gather kernels (bl_tma.cuh)
+      static int grid = 0;
+      if (grid == 0) {
+        cudaFuncSetAttribute(k_primal_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+        cudaFuncSetAttribute(k_dual_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+        int dev = 0, sms = 148, occ = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_primal_tma, kTmaThreads, kTmaSmem);
+        grid = sms * (occ < 1 ? 1 : occ);
+      }
+      const TmaMaps& M = *static_cast<const TmaMaps*>(P.tma_host);
+      k_primal_tma<<<grid, kTmaThreads, kTmaSmem, s>>>(P, M);
+      k_dual_tma<<<grid, kTmaThreads, kTmaSmem, s>>>(P, M);
+      return;
+    }
+  }
+#endif
   k_primal<W, false><<<grid_of((const void*)k_primal<W, false>), kBlock, 0, s>>>(P);
   k_dual<W, false><<<grid_of((const void*)k_dual<W, false>), kBlock, 0, s>>>(P);
 }

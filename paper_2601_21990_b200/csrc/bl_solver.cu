@@ -11,7 +11,9 @@
 //   host is not consulted between iterations; it reads the control block
 //   once at the end.
 
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -25,6 +27,13 @@
 
 #include "batchlp_cuda.h"
 #include "bl_device.cuh"
+
+namespace bl {
+// must match bl_tma.cuh
+struct TmaMaps {
+  CUtensorMap y[2], ax[2], x[2], xt, anx, any, anax;
+};
+}  // namespace bl
 
 namespace {
 
@@ -110,6 +119,7 @@ struct bl_ctx {
   bl::Params exec_params{};
   int exec_trace = -1;
   bl::Ctrl* h_ctrl = nullptr;  // pinned
+  bl::TmaMaps maps{};          // TMA descriptors of the current solve's state
 };
 
 namespace {
@@ -260,6 +270,37 @@ int tail_smem_bytes(const bl_problem* p, int cl) {
     worst = std::max(worst, bytes);
   }
   return worst <= (size_t)160 * 1024 ? (int)((worst + 15) / 16 * 16) : 0;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// libcuda link dependency).
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// [rows][32] fp64 tile view of a column-block-tiled matrix, one 256-byte row
+// per box (gather4 moves four such boxes).
+bool tile_map(CUtensorMap* m, const double* base, size_t rows) {
+  auto fn = encode_tiled();
+  if (!fn || rows == 0 || rows > 0xffffffffull) return false;
+  cuuint64_t dims[2] = {32, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {256};
+  cuuint32_t box[2] = {32, 1};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 void free_graph(bl_ctx* ctx) {
@@ -675,6 +716,26 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.grid = use_graph ? grid : grid_loop;
   P.l2_budget = l2_budget;
   P.handover_bytes = (mode_loop == 0) ? kHandoverBytes : 0.0;
+  // TMA-gather kernels for W = 32 (bl_tma.cuh), opt-in with BATCHLP_TMA=1:
+  // measured slower than the register-gather kernels on B200 (the TMA unit's
+  // per-instruction cost dominates 256-byte gathers)
+  P.tma_host = nullptr;
+  {
+    const char* e = std::getenv("BATCHLP_TMA");
+    const bool want = W == 32 && e && e[0] == '1';
+    if (want) {
+      const size_t rn = (size_t)nb * n, rm = (size_t)nb * m;
+      bl::TmaMaps& M = ctx->maps;
+      bool ok = rn > 0 && rm > 0;
+      for (int k = 0; k < 2 && ok; ++k) {
+        ok = ok && tile_map(&M.y[k], P.Y[k], rm) && tile_map(&M.ax[k], P.AX[k], rm) &&
+             tile_map(&M.x[k], P.X[k], rn);
+      }
+      ok = ok && tile_map(&M.xt, P.XT, rn) && tile_map(&M.anx, P.aX, rn) &&
+           tile_map(&M.any, P.aY, rm) && tile_map(&M.anax, P.aAX, rm);
+      if (ok) P.tma_host = &ctx->maps;
+    }
+  }
   P.tail_part = static_cast<double*>(
       ctx->buf[bl_ctx::B_TAIL].ensure(sizeof(double) * 16 * 5 * 32));
   if (std::getenv("BATCHLP_NO_FAST_TAIL")) P.tail_part = nullptr;
