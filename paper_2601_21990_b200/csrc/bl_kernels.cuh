@@ -159,6 +159,55 @@ __device__ __forceinline__ void gather_row(const int* __restrict__ rp,
   }
 }
 
+// The same product with the row metadata read cooperatively: the L lanes of
+// a row group load L consecutive column indices / values with one coalesced
+// access and broadcast them by shuffles, so the gathers of a row wait on one
+// metadata round trip per L nonzeros instead of one per batch (ncu showed the
+// row kernels stalled on the index -> address chain). Same summation order.
+template <int W>
+__device__ __forceinline__ void gather_row_grp(const int* __restrict__ rp,
+                                               const int* __restrict__ ci,
+                                               const double* __restrict__ cv,
+                                               const double* __restrict__ base, int i, int L,
+                                               double (&acc)[Geo<W>::V]) {
+  constexpr int V = Geo<W>::V;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (L - 1);
+  const unsigned mask = L >= 32 ? 0xffffffffu : (((1u << L) - 1u) << (lane & ~(L - 1)));
+  const int p = __ldg(rp + i);
+  const int e = __ldg(rp + i + 1);
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.0;
+  for (int ch = p; ch < e; ch += L) {
+    const int k = ch + gl;
+    int myc = 0;
+    double myv = 0.0;
+    if (k < e) {
+      myc = __ldg(ci + k);
+      myv = __ldg(cv + k);
+    }
+    const int cnt = min(L, e - ch);
+    for (int t = 0; t < cnt; t += 4) {
+      int c[4];
+      double a[4], x[4][V];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        c[q] = __shfl_sync(mask, myc, t + q, L);
+        a[q] = __shfl_sync(mask, myv, t + q, L);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (t + q < cnt) ld_nc<V>(base + (size_t)c[q] * W, x[q]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (t + q < cnt) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[v] = __dadd_rn(acc[v], __dmul_rn(a[q], x[q][v]));
+        }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // deterministic per-column reduction of one work item
 // ---------------------------------------------------------------------------
@@ -275,6 +324,18 @@ constexpr int kPrimalMinCtas = BL_PRIMAL_MIN_CTAS;
 #endif
 constexpr int kDualMinCtas = BL_DUAL_MIN_CTAS;
 
+// Tells an op how many lanes share a row (only ops with a `lanes` member).
+template <class Op>
+__device__ __forceinline__ auto set_lanes_impl(Op& op, int L, int) -> decltype(op.lanes = L, void()) {
+  op.lanes = L;
+}
+template <class Op>
+__device__ __forceinline__ void set_lanes_impl(Op&, int, long) {}
+template <class Op>
+__device__ __forceinline__ void set_lanes(Op& op, int L) {
+  set_lanes_impl(op, L, 0);
+}
+
 // Walks the work items of a persistent row kernel. Op provides:
 //   begin(b, slot0, acc, owner)  per item (owner: holds the matrix's row 0)
 //   row(b, i, slot0, acc)        per row of the group's contiguous chunk
@@ -310,6 +371,7 @@ __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
     if (tid < W) op.stage(b * W + tid, &s_col[tid]);
     __syncthreads();
     op.begin(b, slot0, acc, r == 0 && g == 0, &s_col[li * V]);
+    set_lanes(op, L);
     for (int i = gs; i < ge; ++i) op.row(b, i, slot0, li, acc);
     publish_item<W, NS, LL>(acc, b, r, R, partials, counters, colsum, s0, Kp, red);
   }
@@ -410,6 +472,7 @@ struct PrimalOp {
   const int* cci;
   const double* ccv;
   bool cached = false;
+  int lanes = Geo<W>::L;  // lanes per row group (narrow tail mappings use fewer)
   __device__ PrimalOp(const Params& p, const Ctrl& C) : P(p) {
     crp = P.trp;
     cci = P.tci;
@@ -441,6 +504,7 @@ struct PrimalOp {
       ld_cs<V>(P.aX + idx, ax);
     }
     double aty[V];
+    // (the cooperative-metadata gather measured slower for A' rows: short rows)
     if (cached) gather_row<W, true>(crp, cci, ccv, Ycur + (size_t)b * m * W + li * V, i, aty);
     else gather_row<W>(crp, cci, ccv, Ycur + (size_t)b * m * W + li * V, i, aty);
 #pragma unroll
@@ -486,7 +550,7 @@ __global__ void __launch_bounds__(kBlock, kPrimalMinCtas) k_primal(Params P) {
 // ---------------------------------------------------------------------------
 // dual: AXT = A XT, YT = sigma (s - proj(s)), Y'/AX' = Halpern, sums
 // ---------------------------------------------------------------------------
-template <int W, bool CHECK>
+template <int W, bool CHECK, bool GRP = true>
 struct DualOp {
   static constexpr int V = Geo<W>::V;
   static constexpr int NS = CHECK ? 9 : 3;
@@ -500,6 +564,7 @@ struct DualOp {
   const int* cci;
   const double* ccv;
   bool cached = false;
+  int lanes = Geo<W>::L;
   __device__ DualOp(const Params& p, const Ctrl& C) : P(p) {
     crp = P.rp;
     cci = P.ci;
@@ -536,6 +601,8 @@ struct DualOp {
     }
     double axt[V];
     if (cached) gather_row<W, true>(crp, cci, ccv, P.XT + (size_t)b * n * W + li * V, i, axt);
+    else if (GRP && lanes >= 4)
+      gather_row_grp<W>(crp, cci, ccv, P.XT + (size_t)b * n * W + li * V, i, lanes, axt);
     else gather_row<W>(crp, cci, ccv, P.XT + (size_t)b * n * W + li * V, i, axt);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -584,12 +651,12 @@ struct DualOp {
   }
 };
 
-template <int W, bool CHECK, int LL = 0>
+template <int W, bool CHECK, int LL = 0, bool GRP = true>
 static __device__ void dual_body(const Params& P, const Ctrl& C, double* red) {
   prof_begin(P, K_DUAL);
-  DualOp<W, CHECK> op(P, C);
+  DualOp<W, CHECK, GRP> op(P, C);
   const int nb = (C.active + W - 1) / W;
-  run_rows<W, DualOp<W, CHECK>::NS, LL>(op, P.m, nb, C.Rd, P.partials, P.counters,
+  run_rows<W, DualOp<W, CHECK, GRP>::NS, LL>(op, P.m, nb, C.Rd, P.partials, P.counters,
                                     P.colsum, S_DY2, P.Kp, red);
   prof_end(P, K_DUAL);
 }
@@ -1582,14 +1649,14 @@ __device__ __forceinline__ void loop_rows(const Params& P, const Ctrl& C, double
   if (C.check) {
     primal_body<W, true, LL>(P, C, red);
     sync();
-    dual_body<W, true, LL>(P, C, red);
+    dual_body<W, true, LL, false>(P, C, red);
     sync();
     check_body<W, LL>(P, C, red);
     sync();
   } else {
     primal_body<W, false, LL>(P, C, red);
     sync();
-    dual_body<W, false, LL>(P, C, red);
+    dual_body<W, false, LL, false>(P, C, red);
     sync();
   }
 }
@@ -1757,6 +1824,7 @@ static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* re
     op.cci = t->pci;
     op.ccv = t->pcv;
     op.cached = t->pcached != 0;
+    op.lanes = L;
     double acc[2][V];
 #pragma unroll
     for (int s = 0; s < 2; ++s)
@@ -1775,12 +1843,13 @@ static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* re
   cluster_sync_all();
   {
     prof_begin(P, K_DUAL);
-    DualOp<W, false> op(P, C);
+    DualOp<W, false, false> op(P, C);
     op.col = tail_cols(1) + li * V;
     op.crp = t->drp;
     op.cci = t->dci;
     op.ccv = t->dcv;
     op.cached = t->dcached != 0;
+    op.lanes = L;
     double acc[3][V];
 #pragma unroll
     for (int s = 0; s < 3; ++s)

@@ -6,8 +6,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 tail -1 gpurun_out/smoke.log
 W=scripts/window_profile.py
 timeout 300 python $W c2 64,256,512,1024,100000 > gpurun_out/win.log 2>&1
-timeout 300 python $W c5 64,128 >> gpurun_out/win.log 2>&1
-timeout 300 python $W c3 64,128 >> gpurun_out/win.log 2>&1
+timeout 300 python $W c5 64 >> gpurun_out/win.log 2>&1
+timeout 300 python $W c3 64 >> gpurun_out/win.log 2>&1
 timeout 300 python $W c1 100000 >> gpurun_out/win.log 2>&1
 cat gpurun_out/win.log
 timeout 900 python bench.py > gpurun_out/bench_c2.log 2>&1
