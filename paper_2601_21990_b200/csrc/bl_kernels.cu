@@ -215,6 +215,12 @@ cudaError_t launch_loop_cluster(const Params& P, cudaStream_t s, int tail_smem) 
   return e;
 }
 
+cudaError_t launch_tail_fast(const Params& P, cudaStream_t s, int tail_smem) {
+  cudaError_t e = cudaSuccess;
+  BL_DISPATCH_W(P.W, e = WLaunch<W_>::tail_fast(P, s, tail_smem));
+  return e;
+}
+
 // Largest cluster (<= 16) of the tail kernel the device can place (cached).
 int max_tail_cluster(int W) {
   static std::mutex mu;

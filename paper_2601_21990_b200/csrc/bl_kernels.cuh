@@ -45,6 +45,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cooperative_groups.h>
+
 #include <map>
 #include <mutex>
 
@@ -58,11 +60,11 @@ namespace bl {
 // LL > 0: "narrow" mapping for the latency-bound tail, where only the first
 // LL * V slots of the (single) active block are live: fewer lanes per row,
 // more rows processed in parallel. The tiled layout (stride W) is unchanged.
-template <int W, int LL = 0>
+template <int W, int LL = 0, int NT = kBlock>
 struct Geo {
   static constexpr int V = W >= 2 ? 2 : 1;                      // slots per lane (double2)
   static constexpr int L = LL > 0 ? LL : (W >= 2 ? W / 2 : 1);  // lanes per row
-  static constexpr int G = kBlock / L;                          // row groups per CTA
+  static constexpr int G = NT / L;                              // row groups per CTA
 };
 
 template <int V>
@@ -149,13 +151,31 @@ __device__ __forceinline__ void gather_row(const int* __restrict__ rp,
       acc[v] = __dadd_rn(acc[v], __dmul_rn(a3, x3[v]));
     }
   }
-  for (; p < e; ++p) {
-    const int c0 = ldi(ci + p);
-    const double a0 = ldd(cv + p);
-    double x0[V];
-    ld_nc<V>(base + (size_t)c0 * W, x0);
+  if constexpr (GENERIC) {  // the tail's cached rows: registers are scarce there
+    for (; p < e; ++p) {
+      const int c0 = ldi(ci + p);
+      const double a0 = ldd(cv + p);
+      double x0[V];
+      ld_nc<V>(base + (size_t)c0 * W, x0);
 #pragma unroll
-    for (int v = 0; v < V; ++v) acc[v] = __dadd_rn(acc[v], __dmul_rn(a0, x0[v]));
+      for (int v = 0; v < V; ++v) acc[v] = __dadd_rn(acc[v], __dmul_rn(a0, x0[v]));
+    }
+  } else if (p < e) {  // remainder (1..3): one predicated batch, loads issued together
+    double a[3] = {0.0, 0.0, 0.0}, x[3][V];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (p + k < e) {
+        a[k] = ldd(cv + p + k);
+        ld_nc<V>(base + (size_t)ldi(ci + p + k) * W, x[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (p + k < e) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] = __dadd_rn(acc[v], __dmul_rn(a[k], x[k][v]));
+      }
+    }
   }
 }
 
@@ -459,7 +479,8 @@ __device__ __forceinline__ void stage_col(const Params& P, int j, int active, bo
 // ---------------------------------------------------------------------------
 // primal: XT = proj(X - tau (c + A'Y)), X' = Halpern, sums
 // ---------------------------------------------------------------------------
-template <int W, bool CHECK>
+// GEN: the CSR arrays may be the tail's shared-memory cache (generic loads)
+template <int W, bool CHECK, bool GEN = false>
 struct PrimalOp {
   static constexpr int V = Geo<W>::V;
   const Params& P;
@@ -471,7 +492,6 @@ struct PrimalOp {
   const int* crp;                // A' CSR (global, or a shared-memory cache of it)
   const int* cci;
   const double* ccv;
-  bool cached = false;
   int lanes = Geo<W>::L;  // lanes per row group (narrow tail mappings use fewer)
   __device__ PrimalOp(const Params& p, const Ctrl& C) : P(p) {
     crp = P.trp;
@@ -505,8 +525,7 @@ struct PrimalOp {
     }
     double aty[V];
     // (the cooperative-metadata gather measured slower for A' rows: short rows)
-    if (cached) gather_row<W, true>(crp, cci, ccv, Ycur + (size_t)b * m * W + li * V, i, aty);
-    else gather_row<W>(crp, cci, ccv, Ycur + (size_t)b * m * W + li * V, i, aty);
+    gather_row<W, GEN>(crp, cci, ccv, Ycur + (size_t)b * m * W + li * V, i, aty);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const ColInfo cl = read_col(col + v);
@@ -550,7 +569,7 @@ __global__ void __launch_bounds__(kBlock, kPrimalMinCtas) k_primal(Params P) {
 // ---------------------------------------------------------------------------
 // dual: AXT = A XT, YT = sigma (s - proj(s)), Y'/AX' = Halpern, sums
 // ---------------------------------------------------------------------------
-template <int W, bool CHECK, bool GRP = true>
+template <int W, bool CHECK, bool GRP = true, bool GEN = false>
 struct DualOp {
   static constexpr int V = Geo<W>::V;
   static constexpr int NS = CHECK ? 9 : 3;
@@ -563,7 +582,6 @@ struct DualOp {
   const int* crp;  // A CSR (global, or a shared-memory cache of it)
   const int* cci;
   const double* ccv;
-  bool cached = false;
   int lanes = Geo<W>::L;
   __device__ DualOp(const Params& p, const Ctrl& C) : P(p) {
     crp = P.rp;
@@ -600,7 +618,7 @@ struct DualOp {
       ld_cs<V>(P.aAX + idx, aax);
     }
     double axt[V];
-    if (cached) gather_row<W, true>(crp, cci, ccv, P.XT + (size_t)b * n * W + li * V, i, axt);
+    if (GEN) gather_row<W, true>(crp, cci, ccv, P.XT + (size_t)b * n * W + li * V, i, axt);
     else if (GRP && lanes >= 4)
       gather_row_grp<W>(crp, cci, ccv, P.XT + (size_t)b * n * W + li * V, i, lanes, axt);
     else gather_row<W>(crp, cci, ccv, P.XT + (size_t)b * n * W + li * V, i, axt);
@@ -1697,6 +1715,7 @@ __device__ __forceinline__ int pass_lanes(int active) {
 //    cluster barrier publishes them and warp 0 of CTA 0 folds them in CTA
 //    order inside a warp-synchronous decide.
 struct TailRows {
+  unsigned long long mark;  // last tail timing mark (CTA 0, BATCHLP_TAIL_TRACE)
   int pr0, pr1, dr0, dr1;  // A' rows (primal) and A rows (dual) of this CTA
   int pcached, dcached;    // metadata in shared memory?
   const int *prp, *pci, *drp, *dci;
@@ -1710,6 +1729,24 @@ static __device__ __noinline__ SColInfo* tail_cols(int which) {
 static __device__ __noinline__ TailRows* tail_rows() {
   __shared__ TailRows t;
   return &t;
+}
+// Diagnostic timing of the fast tail schedule (P.dbg, BATCHLP_TAIL_TRACE):
+// CTA 0 accumulates the %globaltimer time spent between marks k-1 and k.
+__device__ __forceinline__ void tail_mark(const Params& P, int k) {
+  if (P.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+    TailRows* t = tail_rows();
+    const unsigned long long now = gtime();
+    if (k > 0) P.dbg[k] += now - t->mark;
+    else P.dbg[0] += 1;
+    t->mark = now;
+  }
+}
+
+// [cluster CTA][5 sums][32 slots]: per-CTA partials of a fast tail pass,
+// written into CTA 0's copy through distributed shared memory.
+static __device__ __noinline__ double* tail_part_smem() {
+  __shared__ double t[16 * 5 * 32];
+  return t;
 }
 static __device__ __noinline__ Ctrl* tail_ctrl() {
   __shared__ Ctrl c;
@@ -1777,10 +1814,13 @@ static __device__ void tail_setup(const Params& P, char* dyn, int dyn_bytes) {
 
 // Sums of this CTA's rows for NS columns-sums, reduced over the CTA in a
 // fixed tree and stored to P.tail_part[cta][k0 + s][jj].
-template <int W, int NS, int LL>
+template <int W, int NS, int LL, int NT>
 __device__ __forceinline__ void tail_publish(const Params& P, double (&acc)[NS][Geo<W>::V],
                                              int k0, double* red) {
-  using Gm = Geo<W, LL>;
+  using Gm = Geo<W, LL, NT>;
+  constexpr int NW = NT / 32;
+  // CTA 0's partial array, through distributed shared memory
+  double* dst = cooperative_groups::this_cluster().map_shared_rank(tail_part_smem(), 0);
   constexpr int V = Gm::V, L = Gm::L;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #pragma unroll
@@ -1797,33 +1837,32 @@ __device__ __forceinline__ void tail_publish(const Params& P, double (&acc)[NS][
       for (int v = 0; v < V; ++v) red[(warp * NS + s) * W + lane * V + v] = acc[s][v];
   }
   __syncthreads();
-  for (int t = tid; t < NS * W; t += kBlock) {
+  for (int t = tid; t < NS * W; t += NT) {
     const int s = t / W, jj = t - s * W;
     double sum = 0.0;
     if (jj < L * V) {
 #pragma unroll
-      for (int wp = 0; wp < kWarps; ++wp) sum = __dadd_rn(sum, red[(wp * NS + s) * W + jj]);
+      for (int wp = 0; wp < NW; ++wp) sum = __dadd_rn(sum, red[(wp * NS + s) * W + jj]);
     }
-    P.tail_part[((size_t)blockIdx.x * 5 + k0 + s) * 32 + jj] = sum;
+    dst[(blockIdx.x * 5 + k0 + s) * 32 + jj] = sum;
   }
   __syncthreads();
 }
 
-template <int W, int LL>
+template <int W, int LL, int NT>
 static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* red) {
-  using Gm = Geo<W, LL>;
+  using Gm = Geo<W, LL, NT>;
   constexpr int V = Gm::V, L = Gm::L, G = Gm::G;
   const TailRows* t = tail_rows();
   const int tid = threadIdx.x, g = tid / L, li = tid - g * L;
   const bool tiny_n = P.n <= kTinyRows, tiny_m = P.m <= kTinyRows;
   {
     prof_begin(P, K_PRIMAL);
-    PrimalOp<W, false> op(P, C);
+    PrimalOp<W, false, true> op(P, C);
     op.col = tail_cols(0) + li * V;
     op.crp = t->prp;
     op.cci = t->pci;
     op.ccv = t->pcv;
-    op.cached = t->pcached != 0;
     op.lanes = L;
     double acc[2][V];
 #pragma unroll
@@ -1837,18 +1876,20 @@ static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* re
     } else {
       for (int i = r0 + g; i < r1; i += G) op.row(0, i, 0, li, acc);
     }
-    tail_publish<W, 2, LL>(P, acc, 0, red);
+    tail_mark(P, 2);
+    tail_publish<W, 2, LL, NT>(P, acc, 0, red);
     prof_end(P, K_PRIMAL);
+    tail_mark(P, 3);
   }
   cluster_sync_all();
+  tail_mark(P, 4);
   {
     prof_begin(P, K_DUAL);
-    DualOp<W, false, false> op(P, C);
+    DualOp<W, false, false, true> op(P, C);
     op.col = tail_cols(1) + li * V;
     op.crp = t->drp;
     op.cci = t->dci;
     op.ccv = t->dcv;
-    op.cached = t->dcached != 0;
     op.lanes = L;
     double acc[3][V];
 #pragma unroll
@@ -1862,10 +1903,13 @@ static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* re
     } else {
       for (int i = r0 + g; i < r1; i += G) op.row(0, i, 0, li, acc);
     }
-    tail_publish<W, 3, LL>(P, acc, 2, red);
+    tail_mark(P, 5);
+    tail_publish<W, 3, LL, NT>(P, acc, 2, red);
     prof_end(P, K_DUAL);
+    tail_mark(P, 6);
   }
   cluster_sync_all();
+  tail_mark(P, 7);
 }
 
 // decide_body's logic for a plain pass (no check) with active <= 32, run
@@ -1889,12 +1933,12 @@ static __device__ void tail_decide(const Params& P) {
   if (lane < active) {
     // fold the CTA partials in CTA order (sequential, fixed)
     for (int c = 0; c < cl; ++c) {
-      const double* tp = P.tail_part + (size_t)c * 5 * 32 + lane;
-      dx2 = __dadd_rn(dx2, __ldcg(tp));
-      xa2 = __dadd_rn(xa2, __ldcg(tp + 32));
-      dy2 = __dadd_rn(dy2, __ldcg(tp + 64));
-      cross = __dadd_rn(cross, __ldcg(tp + 96));
-      ya2 = __dadd_rn(ya2, __ldcg(tp + 128));
+      const double* tp = tail_part_smem() + c * 5 * 32 + lane;
+      dx2 = __dadd_rn(dx2, tp[0]);
+      xa2 = __dadd_rn(xa2, tp[32]);
+      dy2 = __dadd_rn(dy2, tp[64]);
+      cross = __dadd_rn(cross, tp[96]);
+      ya2 = __dadd_rn(ya2, tp[128]);
     }
     csr(P, S_DX2, lane) = dx2;
     csr(P, S_XA2, lane) = xa2;
@@ -1982,8 +2026,8 @@ static __device__ void tail_decide(const Params& P) {
   }
 }
 
-// One fast tail pass on the cluster (all CTAs).
-template <int W>
+// One fast tail pass on the cluster (all CTAs of NT threads).
+template <int W, int NT = kBlock>
 static __device__ void tail_pass(const Params& P, const Ctrl& C, double* red) {
   TailRows* t = tail_rows();
   if (t->epoch != C.col_epoch) {  // uniform across the CTA
@@ -1997,9 +2041,38 @@ static __device__ void tail_pass(const Params& P, const Ctrl& C, double* red) {
     __syncthreads();
   }
   const int Lsel = pass_lanes<W>(C.active);
-  BL_DISPATCH_L(W, Lsel, (tail_rows_pass<W, LL_>(P, C, red)));
+  tail_mark(P, 1);
+  BL_DISPATCH_L(W, Lsel, (tail_rows_pass<W, LL_, NT>(P, C, red)));
   if (blockIdx.x == 0 && threadIdx.x < 32) tail_decide(P);
+  tail_mark(P, 8);
   cluster_sync_all();
+  tail_mark(P, 9);
+}
+
+// Whether the next pass can take the fast tail schedule.
+__device__ __forceinline__ bool tail_fast_ok(const Params& P, const Ctrl& C, int W) {
+  return (C.active + W - 1) / W == 1 && C.active <= 32 && !C.check && !P.trace && !P.avg_all &&
+         P.tail_part != nullptr;
+}
+
+// Dedicated fast-tail kernel: one cluster of kTailThreads-thread CTAs runs
+// plain tail passes until a pass needs the generic schedule (termination
+// check, certificate, compaction) or the solve is done; the generic cluster
+// kernel then runs that one pass (single-pass mode) and the tail graph loops
+// (bl_solver.cu). More threads per CTA than the generic kernel: more row
+// groups, so fewer rows per group in a pass.
+constexpr int kTailThreads = 512;
+template <int W>
+__global__ void __launch_bounds__(kTailThreads, 1) k_tail_fast(Params P, int tail_smem) {
+  __shared__ double red[(kTailThreads / 32) * 3 * 32];
+  extern __shared__ __align__(16) char tail_dyn[];
+  tail_setup(P, tail_dyn, tail_smem);
+  for (;;) {
+    tail_mark(P, 0);
+    const Ctrl C = load_ctrl(P.ctrl);
+    if (C.done || !tail_fast_ok(P, C, W)) break;
+    tail_pass<W, kTailThreads>(P, C, red);
+  }
 }
 
 // CL = false: cooperative grid over all SMs (grid barriers); it hands over
@@ -2012,7 +2085,8 @@ __global__ void __launch_bounds__(kBlock) k_loop(Params P, int tail_smem) {
   __shared__ double red[kRedDoubles];
   extern __shared__ __align__(16) char tail_dyn[];
   unsigned long long target = 0;
-  if constexpr (CL) tail_setup(P, tail_dyn, tail_smem);
+  (void)tail_dyn;
+  (void)tail_smem;
   auto sync = [&]() {
     if constexpr (CL) cluster_sync_all();
     else grid_sync(P.barrier, target);
@@ -2023,12 +2097,7 @@ __global__ void __launch_bounds__(kBlock) k_loop(Params P, int tail_smem) {
     if (C.done) break;
     const int nba = (C.active + W - 1) / W;
     if (!CL && P.tail_blocks > 0 && nba <= P.tail_blocks) break;
-    if constexpr (CL) {
-      if (nba == 1 && C.active <= 32 && !C.check && !P.trace && !P.avg_all && P.tail_part) {
-        tail_pass<W>(P, C, red);
-        continue;
-      }
-    }
+
     // work decomposition for THIS launch's grid (the control block may have
     // been written by a driver with another grid)
     C.Rp = items_per_block(P.n, P.m, W, grid, nba, P.l2_budget);
@@ -2057,6 +2126,16 @@ __global__ void __launch_bounds__(kBlock) k_loop(Params P, int tail_smem) {
     if (C.hash_pending) {
       if (blockIdx.x == 0 && threadIdx.x == 0) trace_body(P);
       sync();
+    }
+    if constexpr (CL) {
+      if (P.tail_single) break;  // one generic pass between fast-tail launches
+    }
+  }
+  if constexpr (CL) {
+    // tail graph: loop again (fast tail kernel, then this kernel) unless done
+    if (P.tail_single && blockIdx.x == 0 && threadIdx.x == 0) {
+      const Ctrl Cf = load_ctrl(P.ctrl);
+      cudaGraphSetConditional(P.h_tail, Cf.done ? 0u : 1u);
     }
   }
 }
@@ -2123,6 +2202,7 @@ struct WLaunch {
   static cudaError_t loop_cluster(const Params& P, cudaStream_t s, int tail_smem);
   static int max_tail_cluster();
   static int row_ctas_per_sm();
+  static cudaError_t tail_fast(const Params& P, cudaStream_t s, int tail_smem);
 };
 
 // Each row kernel is launched with SMs x (its own max resident CTAs, <= 4):
@@ -2265,6 +2345,34 @@ int WLaunch<W>::max_tail_cluster() {
   }
   cudaGetLastError();
   return best;
+}
+
+// The fast-tail kernel as one cluster of P.grid CTAs of kTailThreads threads.
+template <int W>
+cudaError_t WLaunch<W>::tail_fast(const Params& P, cudaStream_t s, int tail_smem) {
+  cudaError_t e = cudaSuccess;
+  auto fn = k_tail_fast<W>;
+  if (P.grid > 8) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  if (tail_smem > 0) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tail_smem);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P.grid);
+  cfg.blockDim = dim3(kTailThreads);
+  cfg.dynamicSmemBytes = tail_smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = P.grid;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, P, tail_smem);
 }
 
 // Resident CTAs per SM of the widest row kernels (grid of the plain kernels).

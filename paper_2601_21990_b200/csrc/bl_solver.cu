@@ -104,7 +104,7 @@ struct bl_ctx {
     B_RC, B_R, B_DR, B_AXT, B_BX, B_BY, B_BR, B_RX, B_RY, B_RR, B_RDX, B_RDY, B_RDR,
     B_SLOTD, B_SLOTI, B_ORIGI, B_RES, B_COLSUM, B_PART, B_CNT, B_SNAP, B_MOVES,
     B_LOG, B_CTRL, B_PROF, B_PROFACC, B_BAR, B_OV, B_OVD, B_WARMX, B_WARMY, B_PI, B_TMP0, B_TMP1,
-    B_TAIL, B_COUNT
+    B_TAIL, B_DBG, B_COUNT
   };
   DevBuf buf[B_COUNT];
   // last solve
@@ -120,6 +120,11 @@ struct bl_ctx {
   int exec_trace = -1;
   bl::Ctrl* h_ctrl = nullptr;  // pinned
   bl::TmaMaps maps{};          // TMA descriptors of the current solve's state
+  // tail graph cache
+  cudaGraphExec_t tail_exec = nullptr;
+  cudaGraph_t tail_graph = nullptr;
+  bl::Params tail_params{};
+  int tail_smem = -1;
 };
 
 namespace {
@@ -402,7 +407,47 @@ bool same_params(const bl::Params& a, const bl::Params& b) {
   x.use_graph = y.use_graph = 0;
   x.h_loop = y.h_loop = x.h_check = y.h_check = x.h_cert = y.h_cert = 0;
   x.h_snap = y.h_snap = x.h_trace = y.h_trace = 0;
+  x.h_tail = y.h_tail = 0;
   return std::memcmp(&x, &y, sizeof(bl::Params)) == 0;
+}
+
+void free_tail_graph(bl_ctx* ctx) {
+  if (ctx->tail_exec) cudaGraphExecDestroy(ctx->tail_exec);
+  if (ctx->tail_graph) cudaGraphDestroy(ctx->tail_graph);
+  ctx->tail_exec = nullptr;
+  ctx->tail_graph = nullptr;
+  ctx->tail_smem = -1;
+}
+
+// The tail as a device-driven loop: WHILE(not done) { fast-tail cluster
+// kernel (plain passes); generic cluster kernel (exactly one pass: check,
+// certificate, compaction, restart bookkeeping) } — the generic kernel sets
+// the WHILE condition, so the host is not consulted between iterations.
+void run_tail_graph(bl_ctx* ctx, const bl::Params& Q, int smem) {
+  if (!ctx->tail_exec || ctx->tail_smem != smem || !same_params(ctx->tail_params, Q)) {
+    free_tail_graph(ctx);
+    cudaGraph_t g;
+    ck(cudaGraphCreate(&g, 0), "cudaGraphCreate(tail)");
+    cudaGraphConditionalHandle h;
+    ck(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault), "tail handle");
+    cudaGraph_t body;
+    add_cond(g, nullptr, 0, h, cudaGraphCondTypeWhile, 1, &body);
+    cudaStream_t s2 = ctx->side;
+    bl::Params F = Q, G = Q;
+    F.tail_single = 0;
+    F.h_tail = h;
+    G.tail_single = 1;
+    G.h_tail = h;
+    capture_into(s2, body, [&] {
+      ck(bl::launch_tail_fast(F, s2, smem), "tail fast launch");
+      ck(bl::launch_loop_cluster(G, s2, smem), "tail generic launch");
+    });
+    ck(cudaGraphInstantiate(&ctx->tail_exec, g, 0), "cudaGraphInstantiate(tail)");
+    ctx->tail_graph = g;
+    ctx->tail_params = Q;
+    ctx->tail_smem = smem;
+  }
+  ck(cudaGraphLaunch(ctx->tail_exec, ctx->stream), "cudaGraphLaunch(tail)");
 }
 
 void run_loop_graph(bl_ctx* ctx, const bl::Params& P) {
@@ -739,6 +784,12 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.tail_part = static_cast<double*>(
       ctx->buf[bl_ctx::B_TAIL].ensure(sizeof(double) * 16 * 5 * 32));
   if (std::getenv("BATCHLP_NO_FAST_TAIL")) P.tail_part = nullptr;
+  P.dbg = nullptr;
+  if (std::getenv("BATCHLP_TAIL_TRACE")) {
+    P.dbg = static_cast<unsigned long long*>(
+        ctx->buf[bl_ctx::B_DBG].ensure(sizeof(unsigned long long) * 16));
+    ck(cudaMemsetAsync(P.dbg, 0, sizeof(unsigned long long) * 16, s), "dbg");
+  }
   P.barrier = static_cast<unsigned long long*>(
       ctx->buf[bl_ctx::B_BAR].ensure(sizeof(unsigned long long)));
   ck(cudaMemsetAsync(P.barrier, 0, sizeof(unsigned long long), s), "barrier");
@@ -820,8 +871,12 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
         Q.handover_bytes = 0.0;
         Q.use_graph = 0;
         Q.tail_blocks = 0;
-        ck(bl::launch_loop_cluster(Q, s, tail_smem_bytes(p, tail_cluster)),
-           "cluster loop launch");
+        Q.tail_single = 0;
+        const int smem = tail_smem_bytes(p, tail_cluster);
+        const bool fast_tail = P.tail_part && !P.trace && !P.avg_all && W <= 32 &&
+                               !std::getenv("BATCHLP_NO_TAIL_GRAPH");
+        if (fast_tail) run_tail_graph(ctx, Q, smem);
+        else ck(bl::launch_loop_cluster(Q, s, smem), "cluster loop launch");
       }
     }
   }
@@ -838,6 +893,16 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   ck(cudaMemcpyAsync(hacc, P.prof_acc, sizeof(hacc), cudaMemcpyDeviceToHost, s), "prof acc");
   ck(cudaEventRecord(ctx->ev1, s), "event");
   ck(cudaStreamSynchronize(s), "solve sync");
+  if (P.dbg) {
+    unsigned long long d[16];
+    cudaMemcpy(d, P.dbg, sizeof(d), cudaMemcpyDeviceToHost);
+    const double passes = d[0] > 0 ? (double)d[0] : 1.0;
+    static const char* what[] = {"", "top->rows", "primal rows", "primal publish", "primal sync",
+                                 "dual rows", "dual publish", "dual sync", "decide", "final sync"};
+    std::fprintf(stderr, "[tail trace] %llu loop tops\n", (unsigned long long)d[0]);
+    for (int k = 1; k < 10; ++k)
+      std::fprintf(stderr, "[tail trace] %-16s %8.3f us/pass\n", what[k], d[k] / passes / 1e3);
+  }
   const bl::Ctrl C = *ctx->h_ctrl;
   if (C.error == BL_ERR_DOMAIN)
     raise(BL_ERR_DOMAIN,
@@ -950,6 +1015,7 @@ void bl_ctx_destroy(bl_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   free_graph(ctx);
+  free_tail_graph(ctx);
   for (auto& b : ctx->buf) b.release();
   if (ctx->h_ctrl) cudaFreeHost(ctx->h_ctrl);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);

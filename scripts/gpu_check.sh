@@ -12,3 +12,7 @@ timeout 300 python $W c1 100000 >> gpurun_out/win.log 2>&1
 cat gpurun_out/win.log
 timeout 900 python bench.py > gpurun_out/bench_c2.log 2>&1
 tail -1 gpurun_out/bench_c2.log | cut -c1-300
+mkdir -p gpurun_out
+BATCHLP_TAIL_TRACE=1 timeout 300 python scripts/run_config.py c2 1 > gpurun_out/tt.log 2>&1
+BATCHLP_TAIL_TRACE=1 timeout 300 python scripts/run_config.py c1 1 >> gpurun_out/tt.log 2>&1
+cat gpurun_out/tt.log
