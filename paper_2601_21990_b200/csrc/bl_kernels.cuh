@@ -1752,6 +1752,29 @@ static __device__ __noinline__ Ctrl* tail_ctrl() {
   __shared__ Ctrl c;
   return &c;
 }
+// Every CTA's copy of the control block during fast tail passes: CTA 0's
+// decide writes the new state into all of them through distributed shared
+// memory, so a pass starts without a global-memory round trip.
+static __device__ __noinline__ Ctrl* tail_ctrl_in() {
+  __shared__ Ctrl c;
+  return &c;
+}
+
+// Copies CTA 0's decided control block into every CTA's tail_ctrl_in
+// (called by the 32 lanes of warp 0 of CTA 0).
+static __device__ void tail_broadcast_ctrl(int lane) {
+  constexpr int kWords = (int)(sizeof(Ctrl) / 8);
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(tail_ctrl());
+  auto cluster = cooperative_groups::this_cluster();
+  const int cl = (int)cluster.num_blocks();
+  __syncwarp();
+  for (int k = lane; k < cl * kWords; k += 32) {
+    const int rank = k / kWords, word = k - rank * kWords;
+    unsigned long long* dst =
+        reinterpret_cast<unsigned long long*>(cluster.map_shared_rank(tail_ctrl_in(), rank));
+    dst[word] = src[word];
+  }
+}
 
 // Copies rows [r0, r1) of a CSR into shared memory at *cursor; returns
 // pointers offset so that they can be indexed with global row / nonzero
@@ -1917,7 +1940,7 @@ static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* re
 static __device__ void tail_decide(const Params& P) {
   const int lane = threadIdx.x;
   Ctrl& C = *tail_ctrl();
-  if (lane == 0) C = *P.ctrl;
+  if (lane == 0) C = *tail_ctrl_in();
   __syncwarp();
   {
     unsigned long long now = 0;
@@ -1964,6 +1987,7 @@ static __device__ void tail_decide(const Params& P) {
       C.done = 1;
       *P.ctrl = C;
     }
+    tail_broadcast_ctrl(lane);
     return;
   }
   // averaged residual: sequential sum in slot order (ordered_sum, count <= 256)
@@ -2024,6 +2048,7 @@ static __device__ void tail_decide(const Params& P) {
     *P.ctrl = C;
     if (P.prof) atomicMax(&P.prof[2 * K_DECIDE + 1], gtime());
   }
+  tail_broadcast_ctrl(lane);
 }
 
 // One fast tail pass on the cluster (all CTAs of NT threads).
@@ -2067,9 +2092,11 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail_fast(Params P, int tai
   __shared__ double red[(kTailThreads / 32) * 3 * 32];
   extern __shared__ __align__(16) char tail_dyn[];
   tail_setup(P, tail_dyn, tail_smem);
+  if (threadIdx.x == 0) *tail_ctrl_in() = load_ctrl(P.ctrl);
+  __syncthreads();
   for (;;) {
     tail_mark(P, 0);
-    const Ctrl C = load_ctrl(P.ctrl);
+    const Ctrl C = *tail_ctrl_in();
     if (C.done || !tail_fast_ok(P, C, W)) break;
     tail_pass<W, kTailThreads>(P, C, red);
   }
