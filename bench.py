@@ -284,18 +284,21 @@ def main():
     n_ov = len(my_batch.overrides())
     per_solve_h2d = n_ov * 24 + my_batch.batch_width() * (8 * 19 + 4 * 7 + 4 * 3) + 256
     per_solve_d2h = my_batch.batch_width() * (80 + 4) + 256
+    # One long-lived workspace, as a solver process keeps its device context;
+    # every step still uploads the problem from pinned host memory, recomputes
+    # the step size (device power iteration) and reads the per-LP results back.
     e2e_walls = []
-    s = bl.solve_batch(e2e_batch, cfg, my_presets, BatchWorkspace(local),
-                       vectors=bl.Vectors.NONE, cache_problem=False)  # warm-up
+    wse = BatchWorkspace(local)
+    s = bl.solve_batch(e2e_batch, cfg, my_presets, wse, vectors=bl.Vectors.NONE,
+                       cache_problem=False)  # warm-up
     for _ in range(args.steps):
         flush_l2(torch, dev)
         barrier()
-        wse = BatchWorkspace(local)
         t0 = time.perf_counter()
         s = bl.solve_batch(e2e_batch, cfg, my_presets, wse, vectors=bl.Vectors.NONE,
                            cache_problem=False)
         e2e_walls.append(time.perf_counter() - t0)
-        wse.ctx.close()
+    wse.ctx.close()
     e2e_s = sum(e2e_walls) / len(e2e_walls)
     if world > 1:
         t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)

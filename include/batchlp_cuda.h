@@ -181,6 +181,16 @@ int bl_problem_upload(bl_ctx* ctx, int32_t m, int32_t n, int64_t nnz,
                       const double* var_upper, const double* row_lower,
                       const double* row_upper, bl_problem** out);
 void bl_problem_free(bl_problem* p);
+/* Re-fills an uploaded problem with new arrays (same meaning as
+ * bl_problem_upload). Device buffers only grow, so re-uploading a problem
+ * of the same size keeps every device address and the solver's captured
+ * CUDA graphs are reused; the cached spectral norm is invalidated. */
+int bl_problem_assign(bl_ctx* ctx, bl_problem* p, int32_t m, int32_t n, int64_t nnz,
+                      const int32_t* rowptr, const int32_t* col, const double* val,
+                      const int32_t* t_rowptr, const int32_t* t_col,
+                      const double* t_val, const double* objective,
+                      const double* var_lower, const double* var_upper,
+                      const double* row_lower, const double* row_upper);
 
 /* ---- sparse helpers (sparse.hpp) -----------------------------------------
  * spectral_norm (sparse.hpp:297-319): ||A||_2 estimate x 1.01, computed by

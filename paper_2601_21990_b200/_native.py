@@ -147,6 +147,11 @@ SIGNATURES = {
          _DP, _DP, _DP, _DP, _DP, C.POINTER(_P)],
     ),
     "bl_problem_free": (None, [_P]),
+    "bl_problem_assign": (
+        C.c_int,
+        [_P, _P, C.c_int32, C.c_int32, C.c_int64, _IP, _IP, _DP, _IP, _IP, _DP,
+         _DP, _DP, _DP, _DP, _DP],
+    ),
     "bl_spectral_norm": (C.c_int, [_P, _P, _DP]),
     "bl_spmm": (C.c_int, [_P, _P, C.c_int, C.c_int32, C.c_int32, _DP, _DP]),
     "bl_solve_batch": (

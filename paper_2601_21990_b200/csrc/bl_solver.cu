@@ -1029,16 +1029,14 @@ const char* bl_last_error(const bl_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_create_error.c_str();
 }
 
-int bl_problem_upload(bl_ctx* ctx, int32_t m, int32_t n, int64_t nnz,
-                      const int32_t* rowptr, const int32_t* col, const double* val,
-                      const int32_t* t_rowptr, const int32_t* t_col,
-                      const double* t_val, const double* objective,
-                      const double* var_lower, const double* var_upper,
-                      const double* row_lower, const double* row_upper,
-                      bl_problem** out) {
-  *out = nullptr;
-  bl_problem* p = new bl_problem();
-  const int rc = guarded(ctx, [&] {
+namespace {
+// Fills `p` (grow-only buffers: a re-upload of a problem of the same size
+// keeps every device address, so captured CUDA graphs stay valid).
+void fill_problem(bl_ctx* ctx, bl_problem* p, int32_t m, int32_t n, int64_t nnz,
+                  const int32_t* rowptr, const int32_t* col, const double* val,
+                  const int32_t* t_rowptr, const int32_t* t_col, const double* t_val,
+                  const double* objective, const double* var_lower, const double* var_upper,
+                  const double* row_lower, const double* row_upper) {
     if (m < 0 || n < 0 || nnz < 0) raise(BL_ERR_INVALID_ARGUMENT, "sparse: negative dimension");
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
     cudaStream_t s = ctx->stream;
@@ -1061,7 +1059,23 @@ int bl_problem_upload(bl_ctx* ctx, int32_t m, int32_t n, int64_t nnz,
     p->h_rp.assign(rowptr, rowptr + m + 1);
     p->h_trp.assign(t_rowptr, t_rowptr + n + 1);
     p->h_xu.assign(var_upper, var_upper + n);
+    p->norm_valid = false;
     ck(cudaStreamSynchronize(s), "upload sync");
+}
+}  // namespace
+
+int bl_problem_upload(bl_ctx* ctx, int32_t m, int32_t n, int64_t nnz,
+                      const int32_t* rowptr, const int32_t* col, const double* val,
+                      const int32_t* t_rowptr, const int32_t* t_col,
+                      const double* t_val, const double* objective,
+                      const double* var_lower, const double* var_upper,
+                      const double* row_lower, const double* row_upper,
+                      bl_problem** out) {
+  *out = nullptr;
+  bl_problem* p = new bl_problem();
+  const int rc = guarded(ctx, [&] {
+    fill_problem(ctx, p, m, n, nnz, rowptr, col, val, t_rowptr, t_col, t_val, objective,
+                 var_lower, var_upper, row_lower, row_upper);
   });
   if (rc != BL_OK) {
     bl_problem_free(p);
@@ -1069,6 +1083,19 @@ int bl_problem_upload(bl_ctx* ctx, int32_t m, int32_t n, int64_t nnz,
   }
   *out = p;
   return BL_OK;
+}
+
+int bl_problem_assign(bl_ctx* ctx, bl_problem* p, int32_t m, int32_t n, int64_t nnz,
+                      const int32_t* rowptr, const int32_t* col, const double* val,
+                      const int32_t* t_rowptr, const int32_t* t_col,
+                      const double* t_val, const double* objective,
+                      const double* var_lower, const double* var_upper,
+                      const double* row_lower, const double* row_upper) {
+  return guarded(ctx, [&] {
+    if (!p || p->ctx != ctx) raise(BL_ERR_INVALID_ARGUMENT, "assign: problem of another context");
+    fill_problem(ctx, p, m, n, nnz, rowptr, col, val, t_rowptr, t_col, t_val, objective,
+                 var_lower, var_upper, row_lower, row_upper);
+  });
 }
 
 void bl_problem_free(bl_problem* p) {

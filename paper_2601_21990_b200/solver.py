@@ -208,25 +208,39 @@ class DeviceProblem:
     """An LpProblem resident in HBM (bl_problem)."""
 
     def __init__(self, ctx: DeviceContext, p: LpProblem):
+        self.ctx = ctx
+        self.handle = None
+        self.assign(p)
+
+    @staticmethod
+    def _arrays(p: LpProblem):
         A = p.A
         m, n = A.n_rows(), A.n_cols()
         if len(p.objective) != n or p.row_bounds.size() != m or p.var_bounds.size() != n:
             raise InvalidArgument("solve: inconsistent problem dimensions")
-        self._keep = [np.ascontiguousarray(a) for a in (
+        ints = [np.ascontiguousarray(a) for a in (
             A.row_offsets, A.col_indices, A.values, A.t_row_offsets, A.t_col_indices,
             A.t_values)]
         vec = [np.ascontiguousarray(a, dtype=np.float64) for a in (
             p.objective, p.var_bounds.lower, p.var_bounds.upper, p.row_bounds.lower,
             p.row_bounds.upper)]
-        h = C.c_void_p()
-        k = self._keep
-        _check(ctx.handle, N.lib().bl_problem_upload(
-            ctx.handle, m, n, A.nnz(), N.iptr(k[0]), N.iptr(k[1]), N.dptr(k[2]),
-            N.iptr(k[3]), N.iptr(k[4]), N.dptr(k[5]), *[N.dptr(v) for v in vec],
-            C.byref(h)))
-        self._keep = None
-        self.handle = h
-        self.ctx = ctx
+        k = ints
+        args = (m, n, A.nnz(), N.iptr(k[0]), N.iptr(k[1]), N.dptr(k[2]), N.iptr(k[3]),
+                N.iptr(k[4]), N.dptr(k[5]), *[N.dptr(v) for v in vec])
+        return m, n, args, (ints, vec)
+
+    def assign(self, p: LpProblem) -> None:
+        """(Re)uploads p; re-uploading keeps the device buffers (grow-only),
+        so the solver's captured graphs stay valid (bl_problem_assign)."""
+        m, n, args, keep = self._arrays(p)
+        L = N.lib()
+        if self.handle is None:
+            h = C.c_void_p()
+            _check(self.ctx.handle, L.bl_problem_upload(self.ctx.handle, *args, C.byref(h)))
+            self.handle = h
+        else:
+            _check(self.ctx.handle, L.bl_problem_assign(self.ctx.handle, self.handle, *args))
+        del keep
         self.m, self.n = m, n
 
     def close(self) -> None:
@@ -248,12 +262,21 @@ class BatchWorkspace:
     def __init__(self, device: int = 0):
         self.ctx = DeviceContext(device)
         self._problems: Dict[int, tuple] = {}
+        self._scratch: Optional[DeviceProblem] = None
 
     def resident(self, p: LpProblem, cache: bool = True) -> DeviceProblem:
         key = id(p.A)
         hit = self._problems.get(key)
         if cache and hit is not None and hit[0] is p.A and hit[2] is p.objective:
             return hit[1]
+        if not cache:
+            # a fresh upload every call (the caller's arrays may have changed),
+            # into one reusable device problem of this workspace
+            if self._scratch is None:
+                self._scratch = DeviceProblem(self.ctx, p)
+            else:
+                self._scratch.assign(p)
+            return self._scratch
         dp = DeviceProblem(self.ctx, p)
         if cache:
             if len(self._problems) > 8:
@@ -462,7 +485,6 @@ def spmm(A: SparseMatrix, X: np.ndarray, out: Optional[np.ndarray] = None,
     oc = np.ascontiguousarray(out.T)
     _check(ws.ctx.handle, N.lib().bl_spmm(ws.ctx.handle, dp.handle, int(bool(transpose_a)),
                                           width, active, N.dptr(xc), N.dptr(oc)))
-    dp.close()
     out[:, :] = oc.T
     return out
 
