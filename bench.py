@@ -156,7 +156,7 @@ def cpu_sample(name, p, batch, presets, cfg, spec, sample):
     from paper_2601_21990_b200 import distributed as D
     width = batch.batch_width()
     if spec.kind == "obbt":
-        nv = sample or 200
+        nv = sample or 600
         n = p.num_cols()
         cols = list(range(nv)) + list(range(n, n + nv))
     else:
@@ -320,17 +320,25 @@ def main():
     roof = None
     if dom:
         ach = row[dom][2] / row[dom][1]  # bytes/ns == GB/s
-        traffic = None
+        # DRAM traffic of one captured launch of this kernel (ncu --set full,
+        # profiles/ncu_traffic.json), next to that launch's algorithmic bytes:
+        # traffic/alg > 1 would mean wasted re-reads
+        traffic, traffic_launch = None, None
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                tj = json.load(f).get(args.config, {})
-            traffic = tj.get(dom)
+                tj = json.load(f).get(args.config, {}).get(dom)
+            if tj:
+                traffic = tj["traffic"]
+                traffic_launch = {"alg_bytes": tj["alg_bytes"],
+                                  "traffic_over_alg": tj["traffic_over_alg"],
+                                  "ncu_us": tj["ncu_us"], "launch": tj["launch"]}
         except Exception:
             pass
         total_ns = sum(v[1] for v in prof.values())
         roof = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": round(ach, 1),
                 "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic,
+                "traffic_launch": traffic_launch,
                 "alg_bytes_per_launch": round(row[dom][2] / row[dom][0]),
                 "avg_launch_us": round(row[dom][1] / row[dom][0] / 1e3, 3),
                 "share_of_kernel_time": round(row[dom][1] / total_ns, 3) if total_ns else None,

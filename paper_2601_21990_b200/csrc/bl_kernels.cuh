@@ -1382,6 +1382,20 @@ static __device__ void prof_fold(const Params& P, const Ctrl& C, int k, unsigned
     P.prof_acc[3 * K_CHECK + 2] += 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 5.0 * n);
 }
 
+// Diagnostic timing of decide_body on plain passes (P.dbg slots 10-14).
+static __device__ __noinline__ unsigned long long* decide_mark_slot() {
+  __shared__ unsigned long long t;
+  return &t;
+}
+__device__ __forceinline__ void decide_mark(const Params& P, const Ctrl& C, int k) {
+  if (P.dbg && threadIdx.x == 0 && !C.check) {
+    const unsigned long long now = gtime();
+    if (k > 10) P.dbg[k] += now - *decide_mark_slot();
+    else P.dbg[10] += 1;
+    *decide_mark_slot() = now;
+  }
+}
+
 static __device__ void decide_body(const Params& P, int phase) {
   double* scratch = P.scratch;
   __shared__ double sh[kDecideScratchInts / 2];
@@ -1394,6 +1408,7 @@ static __device__ void decide_body(const Params& P, int phase) {
   if (phase == 1 && !C.cert_pending) return;
   const int active = C.active;
   double mean;
+  if (phase == 0) decide_mark(P, C, 10);
   if (phase == 0) {
     if (tid < 32) {
       unsigned long long now = 0;
@@ -1433,6 +1448,7 @@ static __device__ void decide_body(const Params& P, int phase) {
     }
     const int count = P.avg_all ? P.width : active;
     mean = ordered_sum(P.resid, count, sh) / (double)count;
+    decide_mark(P, C, 11);
     if (C.inner_k == 0) {
       for (int j = tid; j < active; j += (int)blockDim.x) P.anchor_resid[j] = P.resid[j];
     }
@@ -1476,8 +1492,10 @@ static __device__ void decide_body(const Params& P, int phase) {
     }
     __syncthreads();
   }
+  if (phase == 0) decide_mark(P, C, 12);
   finalize(P, C, mean, sh, ish, scratch);
   __syncthreads();
+  if (phase == 0) decide_mark(P, C, 13);
   if (tid == 0) {
     if (C.n_snap > 0 || C.n_moves > 0) C.launches += 2;
     if (C.hash_pending) C.launches += 1;

@@ -902,6 +902,11 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
     std::fprintf(stderr, "[tail trace] %llu loop tops\n", (unsigned long long)d[0]);
     for (int k = 1; k < 10; ++k)
       std::fprintf(stderr, "[tail trace] %-16s %8.3f us/pass\n", what[k], d[k] / passes / 1e3);
+    const double dp = d[10] > 0 ? (double)d[10] : 1.0;
+    static const char* dwhat[] = {"resid+mean", "check block", "finalize"};
+    std::fprintf(stderr, "[decide trace] %llu plain passes\n", (unsigned long long)d[10]);
+    for (int k = 11; k < 14; ++k)
+      std::fprintf(stderr, "[decide trace] %-16s %8.3f us/pass\n", dwhat[k - 11], d[k] / dp / 1e3);
   }
   const bl::Ctrl C = *ctx->h_ctrl;
   if (C.error == BL_ERR_DOMAIN)
