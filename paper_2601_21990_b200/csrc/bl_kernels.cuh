@@ -937,19 +937,39 @@ __device__ __forceinline__ DD dd_mul_d(DD a, double b) {
   return fast_two_sum(p, e);
 }
 // exp(x) = 2^k * s, s as a double-double.
+// 1/i as double-doubles (exact to ~2^-106), i = 1..12.
+__device__ __constant__ double kInvDD[12][2] = {
+    {1.0, 0.0},
+    {0.5, 0.0},
+    {0.3333333333333333, 1.850371707708594e-17},
+    {0.25, 0.0},
+    {0.2, -1.1102230246251566e-17},
+    {0.16666666666666666, 9.25185853854297e-18},
+    {0.14285714285714285, 7.93016446160826e-18},
+    {0.125, 0.0},
+    {0.1111111111111111, 6.1679056923619804e-18},
+    {0.1, -5.551115123125783e-18},
+    {0.09090909090909091, -2.523234146875356e-18},
+    {0.08333333333333333, 4.625929269271485e-18},
+};
+// ln 4, correctly rounded (glibc's log(4.0))
+constexpr double kLog4 = 1.3862943611198906;
+
 static __device__ DD dd_exp_scaled(double x, int* k_out) {
   const DD ln2 = {0.6931471805599453, 2.3190468138462996e-17};
   const double k = rint(x / ln2.hi);
   DD r = dd_add({x, 0.0}, dd_mul_d(ln2, -k));
-  r.hi = ldexp(r.hi, -10);
-  r.lo = ldexp(r.lo, -10);
+  // |r| <= ln2/2 / 2^8: 12 Taylor terms reach ~2^-120, 8 squarings lose 8 bits
+  r.hi = ldexp(r.hi, -8);
+  r.lo = ldexp(r.lo, -8);
   DD s = {1.0, 0.0};
-  for (int i = 16; i >= 1; --i) {  // Horner: 1 + r/i * (...)
-    const double inv = 1.0 / i;
-    const DD inv_dd = {inv, __fma_rn(-inv, (double)i, 1.0) / i};
+#pragma unroll
+  for (int i = 12; i >= 1; --i) {  // Horner: 1 + r/i * (...)
+    const DD inv_dd = {kInvDD[i - 1][0], kInvDD[i - 1][1]};
     s = dd_add({1.0, 0.0}, dd_mul(dd_mul(r, inv_dd), s));
   }
-  for (int i = 0; i < 10; ++i) s = dd_mul(s, s);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s = dd_mul(s, s);
   *k_out = (int)k;
   return s;
 }
@@ -982,7 +1002,7 @@ __device__ __forceinline__ double smoothed_weight(double w, double dxn, double d
   if (!isfinite(d) || d <= 0.0) return w;
   const double log_w = cr_log(w);
   const double proposed = theta * cr_log(d) + (1.0 - theta) * log_w;
-  const double step_cap = cr_log(4.0);
+  const double step_cap = kLog4;  // cr_log(4.0)
   if (proposed > log_w + step_cap) return cr_exp(log_w + step_cap);
   if (proposed < log_w - step_cap) return cr_exp(log_w - step_cap);
   return cr_exp(proposed);
@@ -1387,8 +1407,8 @@ static __device__ __noinline__ unsigned long long* decide_mark_slot() {
   __shared__ unsigned long long t;
   return &t;
 }
-__device__ __forceinline__ void decide_mark(const Params& P, const Ctrl& C, int k) {
-  if (P.dbg && threadIdx.x == 0 && !C.check) {
+__device__ __forceinline__ void decide_mark(const Params& P, bool plain, int k) {
+  if (P.dbg && threadIdx.x == 0 && plain) {
     const unsigned long long now = gtime();
     if (k > 10) P.dbg[k] += now - *decide_mark_slot();
     else P.dbg[10] += 1;
@@ -1408,7 +1428,8 @@ static __device__ void decide_body(const Params& P, int phase) {
   if (phase == 1 && !C.cert_pending) return;
   const int active = C.active;
   double mean;
-  if (phase == 0) decide_mark(P, C, 10);
+  const bool plain_pass = !C.check;
+  if (phase == 0) decide_mark(P, plain_pass, 10);
   if (phase == 0) {
     if (tid < 32) {
       unsigned long long now = 0;
@@ -1425,10 +1446,18 @@ static __device__ void decide_body(const Params& P, int phase) {
       if (C.passes > 2 * P.max_it + 1024) ish[3] = 2;
     }
     __syncthreads();
+    // residuals; for a wide batch the strided partial sums of ordered_sum are
+    // accumulated on the fly (same order), saving a reload of resid
+    const int count = P.avg_all ? P.width : active;
+    const bool fused_sum = !P.avg_all && count > 256;
+    double part = 0.0;
+#pragma unroll 4
     for (int j = tid; j < active; j += (int)blockDim.x) {
       int err = 0;
-      P.resid[j] = m_residual(cs(P, S_DX2, j), cs(P, S_DY2, j), cs(P, S_CROSS, j),
-                              P.eta, P.w[j], &err);
+      const double r = m_residual(cs(P, S_DX2, j), cs(P, S_DY2, j), cs(P, S_CROSS, j),
+                                  P.eta, P.w[j], &err);
+      P.resid[j] = r;
+      part += r;
       if (err) ish[3] = 1;
     }
     __syncthreads();
@@ -1446,9 +1475,19 @@ static __device__ void decide_body(const Params& P, int phase) {
       }
       return;
     }
-    const int count = P.avg_all ? P.width : active;
-    mean = ordered_sum(P.resid, count, sh) / (double)count;
-    decide_mark(P, C, 11);
+    if (fused_sum) {
+      sh[tid] = part;
+      __syncthreads();
+      for (int off = (int)blockDim.x / 2; off > 0; off >>= 1) {
+        if (tid < off) sh[tid] = sh[tid] + sh[tid + off];
+        __syncthreads();
+      }
+      mean = sh[0] / (double)count;
+      __syncthreads();
+    } else {
+      mean = ordered_sum(P.resid, count, sh) / (double)count;
+    }
+    decide_mark(P, plain_pass, 11);
     if (C.inner_k == 0) {
       for (int j = tid; j < active; j += (int)blockDim.x) P.anchor_resid[j] = P.resid[j];
     }
@@ -1492,10 +1531,10 @@ static __device__ void decide_body(const Params& P, int phase) {
     }
     __syncthreads();
   }
-  if (phase == 0) decide_mark(P, C, 12);
+  if (phase == 0) decide_mark(P, plain_pass, 12);
   finalize(P, C, mean, sh, ish, scratch);
   __syncthreads();
-  if (phase == 0) decide_mark(P, C, 13);
+  if (phase == 0) decide_mark(P, plain_pass, 13);
   if (tid == 0) {
     if (C.n_snap > 0 || C.n_moves > 0) C.launches += 2;
     if (C.hash_pending) C.launches += 1;
