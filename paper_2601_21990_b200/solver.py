@@ -28,6 +28,16 @@ from .errors import BY_CODE, DeviceError, InvalidArgument
 from .problem import BatchProblem, LpProblem, ObjectiveMode, SparseMatrix, kInf
 
 
+# Shared read-only empty vector: the default of every result vector, so that
+# building K results does not allocate 6K numpy arrays.
+_EMPTY = np.zeros(0)
+_EMPTY.setflags(write=False)
+
+
+def _empty() -> np.ndarray:
+    return _EMPTY
+
+
 class SolveStatus(enum.IntEnum):
     kOptimal = 0
     kPrimalInfeasible = 1
@@ -118,9 +128,14 @@ class Residuals:
 
 @dataclass
 class InfeasibilityProbe:
-    delta_x: np.ndarray = field(default_factory=lambda: np.zeros(0))
-    delta_y: np.ndarray = field(default_factory=lambda: np.zeros(0))
-    delta_r: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    delta_x: np.ndarray = field(default_factory=_empty)
+    delta_y: np.ndarray = field(default_factory=_empty)
+    delta_r: np.ndarray = field(default_factory=_empty)
+
+
+# The (empty) certificate of every result without one; results that carry a
+# certificate get their own InfeasibilityProbe.
+_NO_CERTIFICATE = InfeasibilityProbe()
 
 
 @dataclass
@@ -128,9 +143,9 @@ class SolveResult:
     """solver.hpp:134-145 (plus the device-computed support sums)."""
     status: SolveStatus = SolveStatus.kIterationLimit
     objective: float = math.nan
-    x: np.ndarray = field(default_factory=lambda: np.zeros(0))
-    y: np.ndarray = field(default_factory=lambda: np.zeros(0))
-    reduced_costs: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    x: np.ndarray = field(default_factory=_empty)
+    y: np.ndarray = field(default_factory=_empty)
+    reduced_costs: np.ndarray = field(default_factory=_empty)
     residuals: Residuals = field(default_factory=Residuals)
     iterations: int = 0
     restarts: int = 0
@@ -301,6 +316,44 @@ def default_workspace(device: int = 0) -> BatchWorkspace:
 # ---------------------------------------------------------------------------
 # solve_batch / solve
 # ---------------------------------------------------------------------------
+_STATUS = list(SolveStatus)
+_RESULT_DTYPE = None
+
+
+def _result_view(res, width: int) -> np.ndarray:
+    """Zero-copy structured view of a bl_column_result array."""
+    global _RESULT_DTYPE
+    if _RESULT_DTYPE is None:
+        _RESULT_DTYPE = np.ctypeslib.as_array((N.bl_column_result * 1)()).dtype
+    return np.frombuffer(res, dtype=_RESULT_DTYPE, count=width)
+
+
+def _results_from_c(res, width: int) -> list:
+    """Per-LP SolveResults from the bl_column_result array, via one numpy
+    view (attribute access on 10^3-10^4 ctypes structs dominates otherwise)."""
+    a = _result_view(res, width)
+    c = {name: a[name].tolist() for name in a.dtype.names}
+    new = object.__new__
+    out = []
+    # instances are filled through __dict__ (dataclass __init__ with its
+    # default factories costs microseconds per object)
+    for st, ob, ga, pr, du, fp, it, rs, bs, rw, bb, ve in zip(
+            c["status"], c["objective"], c["gap"], c["primal"], c["dual"], c["fixed_point"],
+            c["iterations"], c["restarts"], c["bound_support"], c["row_support"],
+            c["base_bound_support"], c["vectors_exist"]):
+        res_ = new(Residuals)
+        res_.__dict__.update(gap=ga, primal=pr, dual=du, fixed_point=fp)
+        r = new(SolveResult)
+        r.__dict__.update(status=_STATUS[st], objective=ob, x=_EMPTY, y=_EMPTY,
+                          reduced_costs=_EMPTY, residuals=res_, iterations=it, restarts=rs,
+                          certificate=_NO_CERTIFICATE, restart_log=[],
+                          trajectory_hash=1469598103934665603,
+                          sparse_products=0, bound_support=bs, row_support=rw,
+                          base_bound_support=bb, vectors_exist=bool(ve))
+        out.append(r)
+    return out
+
+
 def _result_from_c(r: N.bl_column_result) -> SolveResult:
     out = SolveResult()
     out.status = SolveStatus(r.status)
@@ -386,19 +439,23 @@ def solve_batch(batch: BatchProblem, cfg: Optional[SolverConfig] = None,
                                         e.residual, e.anchor_residual)
                            for e in ev[:got.value]]
     preset_of = {p.column: p for p in presets}
+    converted = _results_from_c(res, width)
+    a = _result_view(res, width)
+    has_sol = a["has_solution"].tolist()
+    has_cert = a["has_certificate"].tolist()
     for j in range(width):
         if j in preset_of:
             out.per_problem.append(preset_of[j].result)
             continue
-        r = _result_from_c(res[j])
-        if res[j].has_solution:
+        r = converted[j]
+        if has_sol[j]:
             x = np.empty(n)
             y = np.empty(m)
             red = np.empty(n)
             _check(ws.ctx.handle, L.bl_fetch_solution(ws.ctx.handle, j, N.dptr(x), N.dptr(y),
                                                       N.dptr(red)))
             r.x, r.y, r.reduced_costs = x, y, red
-        if res[j].has_certificate:
+        if has_cert[j]:
             dx = np.empty(n)
             dy = np.empty(m)
             dr = np.empty(n)
