@@ -165,9 +165,16 @@ bool interval_valid(double lo, double hi) {  // Interval::valid, bounds.hpp:35-3
          lo <= hi;
 }
 
+// Column-block width: the batch width rounded up to a power of two, at most
+// 32 (BATCHLP_MAX_W lowers the cap for tuning sweeps).
 int pow2_width(int width) {
+  static int cap = [] {
+    const char* e = std::getenv("BATCHLP_MAX_W");
+    const int v = e ? std::atoi(e) : 32;
+    return (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) ? v : 32;
+  }();
   int W = 1;
-  while (W < width && W < 32) W <<= 1;
+  while (W < width && W < cap) W <<= 1;
   return W;
 }
 
