@@ -2310,6 +2310,7 @@ inline int grid_of(const void* fn) {
 }  // namespace bl
 #ifdef BL_WITH_TMA
 #include "bl_tma.cuh"
+#include "bl_slice.cuh"
 #endif
 namespace bl {
 
@@ -2324,6 +2325,21 @@ template <int W>
 void WLaunch<W>::iteration_plain(const Params& P, cudaStream_t s) {
 #ifdef BL_WITH_TMA
   if constexpr (W == 32) {
+    if (P.slice_p.ch > 0) {  // slice-staged kernels (bl_slice.cuh)
+      static int grid = 0;
+      if (grid == 0) {
+        const int mx = 227 * 1024 - 6144;
+        cudaFuncSetAttribute(k_slice<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_slice<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid = sms;
+      }
+      k_slice<false><<<grid, P.slice_p.ch * kSliceLanes, P.slice_p.smem, s>>>(P);
+      k_slice<true><<<grid, P.slice_d.ch * kSliceLanes, P.slice_d.smem, s>>>(P);
+      return;
+    }
     if (P.tma_host) {  // TMA-gather kernels (bl_tma.cuh)
       static int grid = 0;
       if (grid == 0) {

@@ -33,6 +33,7 @@ namespace bl {
 struct TmaMaps {
   CUtensorMap y[2], ax[2], x[2], xt, anx, any, anax;
 };
+
 }  // namespace bl
 
 namespace {
@@ -104,7 +105,7 @@ struct bl_ctx {
     B_RC, B_R, B_DR, B_AXT, B_BX, B_BY, B_BR, B_RX, B_RY, B_RR, B_RDX, B_RDY, B_RDR,
     B_SLOTD, B_SLOTI, B_ORIGI, B_RES, B_COLSUM, B_PART, B_CNT, B_SNAP, B_MOVES,
     B_LOG, B_CTRL, B_PROF, B_PROFACC, B_BAR, B_OV, B_OVD, B_WARMX, B_WARMY, B_PI, B_TMP0, B_TMP1,
-    B_TAIL, B_DBG, B_COUNT
+    B_TAIL, B_DBG, B_SPART, B_SCNT, B_COUNT
   };
   DevBuf buf[B_COUNT];
   // last solve
@@ -194,7 +195,7 @@ int items_for(int rows, int W, int grid) {
 
 template <class T>
 void upload(DevBuf& b, const T* src, size_t count, cudaStream_t s) {
-  b.ensure(count * sizeof(T));
+  b.ensure(count * sizeof(T) + 16);  // the slice kernels copy aligned 16-byte supersets
   if (count) ck(cudaMemcpyAsync(b.p, src, count * sizeof(T), cudaMemcpyHostToDevice, s),
                 "upload");
 }
@@ -303,16 +304,47 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
 
 // [rows][32] fp64 tile view of a column-block-tiled matrix, one 256-byte row
 // per box (gather4 moves four such boxes).
-bool tile_map(CUtensorMap* m, const double* base, size_t rows) {
+bool tile_map(CUtensorMap* m, const double* base, size_t rows, unsigned box_cols = 32,
+              unsigned box_rows = 1) {
   auto fn = encode_tiled();
   if (!fn || rows == 0 || rows > 0xffffffffull) return false;
   cuuint64_t dims[2] = {32, (cuuint64_t)rows};
   cuuint64_t strides[1] = {256};
-  cuuint32_t box[2] = {32, 1};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t es[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Geometry of a slice kernel over `rows` CSR rows (row pointers `h`) that
+// gathers from `rows_in` rows, streaming `na` arrays: the largest chunk that
+// leaves >= 3 pipeline stages in shared memory (else >= 2), the nonzero
+// capacity of any chunk-sized row window (bl_slice.cuh).
+bool slice_geometry(int na, int rows, int rows_in, const std::vector<int>& h, bl::SliceGeo* g) {
+  constexpr int kMaxDyn = 227 * 1024 - 6144;  // minus the kernels' static shared memory
+  const int avail = kMaxDyn - bl::slice_bytes(rows_in) - bl::slice_rp_bytes(rows);
+  if (avail <= 0 || (int)h.size() != rows + 1) return false;
+  int force = 0;
+  if (const char* e = std::getenv("BATCHLP_SLICE_CH")) force = std::atoi(e);
+  int force_st = 0;
+  if (const char* e = std::getenv("BATCHLP_SLICE_STAGES")) force_st = std::atoi(e);
+  for (int need = 3; need >= 2; --need) {
+    for (int ch : {128, 96, 64, 32}) {
+      if (force && ch != force) continue;
+      int nz = 0;
+      for (int i = 0; i < rows; ++i) nz = std::max(nz, h[std::min(rows, i + ch)] - h[i]);
+      nz = (nz + 3) & ~3;
+      const int sb = bl::slice_stage_bytes(na, ch, nz);
+      int st = std::min(bl::kSliceMaxStages, avail / sb);
+      if (force_st) st = std::min(st, force_st);
+      if (st >= need || (force && st >= 2)) {
+        *g = bl::SliceGeo{ch, st, nz, bl::slice_bytes(rows_in) + bl::slice_rp_bytes(rows) + st * sb};
+        return true;
+      }
+    }
+  }
+  return false;
 }
 
 void free_graph(bl_ctx* ctx) {
@@ -787,6 +819,25 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
            tile_map(&M.any, P.aY, rm) && tile_map(&M.anax, P.aAX, rm);
       if (ok) P.tma_host = &ctx->maps;
     }
+  }
+  // slice-staged kernels for W = 32 when an 8-slot sub-slice of either
+  // gathered operand fits in shared memory (bl_slice.cuh), opt-in with
+  // BATCHLP_SLICE=1: measured slower than the register-gather kernels on B200
+  // (one 210 KB CTA per SM leaves 2-3 warps per scheduler)
+  P.slice_part = nullptr;
+  P.slice_cnt = nullptr;
+  P.slice_p = P.slice_d = bl::SliceGeo{0, 0, 0, 0};
+  if (W == 32 && !P.tma_host && m <= bl::kSliceMaxRows && n <= bl::kSliceMaxRows && m > 0 &&
+      n > 0 && std::getenv("BATCHLP_SLICE") && std::getenv("BATCHLP_SLICE")[0] == '1' &&
+      slice_geometry(2, n, m, p->h_trp, &P.slice_p) &&
+      slice_geometry(4, m, n, p->h_rp, &P.slice_d)) {
+    const int nvb = Kp / bl::kSliceCols;
+    P.slice_part = static_cast<double*>(ctx->buf[bl_ctx::B_SPART].ensure(
+        sizeof(double) * (size_t)nvb * bl::kSliceRMax * 3 * bl::kSliceCols));
+    P.slice_cnt = static_cast<int*>(ctx->buf[bl_ctx::B_SCNT].ensure(sizeof(int) * (size_t)nvb));
+    ck(cudaMemsetAsync(P.slice_cnt, 0, sizeof(int) * (size_t)nvb, s), "slice counters");
+  } else {
+    P.slice_p = P.slice_d = bl::SliceGeo{0, 0, 0, 0};
   }
   P.tail_part = static_cast<double*>(
       ctx->buf[bl_ctx::B_TAIL].ensure(sizeof(double) * 16 * 5 * 32));

@@ -147,3 +147,30 @@ def test_tma_gather_kernels_agree_with_reference_c2_prefix(ref, monkeypatch):
         assert abs(g.iterations - w.iterations) <= 0.1 * max(w.iterations, 1)
         if w.status == 0:
             assert abs(g.objective - w.objective) <= 1e-6 * (1 + abs(w.objective))
+
+
+@pytest.mark.parametrize("geometry", ["auto", "128/2", "64/4", "32/2"])
+def test_slice_kernels_agree_with_reference_c2_prefix(ref, geometry, monkeypatch):
+    """The slice-staged kernels (bl_slice.cuh: 8-slot operand sub-slice in
+    shared memory, TMA-pipelined row chunks) at several chunk / stage
+    geometries: C2 OBBT capped at 256 iterations matches the reference."""
+    monkeypatch.setenv("BATCHLP_LOOP", "graph")
+    monkeypatch.setenv("BATCHLP_SLICE", "1")
+    if geometry != "auto":
+        ch, st = geometry.split("/")
+        monkeypatch.setenv("BATCHLP_SLICE_CH", ch)
+        monkeypatch.setenv("BATCHLP_SLICE_STAGES", st)
+    p = I.config_problem("c2")
+    ob = bl.build_obbt_batch(p, bl.ObbtConfig())
+    cfg = bl.ObbtConfig().solver_config()
+    cfg.max_iterations = 256
+    got = bl.solve_batch(ob.batch, cfg, ob.presets, vectors=bl.Vectors.NONE)
+    want = ref.solve_batch(p, ob.batch.batch_width(), 1, [], cfg,
+                           [(q.column, int(q.result.status), q.result.objective)
+                            for q in ob.presets], vectors=False)
+    assert got.iterations == want.iterations
+    for g, w in zip(got.per_problem, want.per_problem):
+        assert int(g.status) == w.status
+        assert abs(g.iterations - w.iterations) <= 0.1 * max(w.iterations, 1)
+        if w.status == 0:
+            assert abs(g.objective - w.objective) <= 1e-6 * (1 + abs(w.objective))
