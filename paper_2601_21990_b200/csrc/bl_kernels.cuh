@@ -2336,8 +2336,20 @@ void WLaunch<W>::iteration_plain(const Params& P, cudaStream_t s) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         grid = sms;
       }
-      k_slice<false><<<grid, P.slice_p.ch * kSliceLanes, P.slice_p.smem, s>>>(P);
-      k_slice<true><<<grid, P.slice_d.ch * kSliceLanes, P.slice_d.smem, s>>>(P);
+      if (P.slice_p.stages == 0) {
+        static bool attr = false;
+        if (!attr) {
+          const int mx = 227 * 1024 - 8192;
+          cudaFuncSetAttribute(k_slice_direct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+          cudaFuncSetAttribute(k_slice_direct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+          attr = true;
+        }
+        k_slice_direct<false><<<grid, kSliceDirectThreads, P.slice_p.smem, s>>>(P);
+        k_slice_direct<true><<<grid, kSliceDirectThreads, P.slice_d.smem, s>>>(P);
+      } else {
+        k_slice<false><<<grid, P.slice_p.ch * kSliceLanes, P.slice_p.smem, s>>>(P);
+        k_slice<true><<<grid, P.slice_d.ch * kSliceLanes, P.slice_d.smem, s>>>(P);
+      }
       return;
     }
     if (P.tma_host) {  // TMA-gather kernels (bl_tma.cuh)

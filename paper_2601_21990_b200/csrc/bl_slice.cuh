@@ -387,4 +387,155 @@ __global__ void __launch_bounds__(kSliceMaxThreads, 1)
   prof_end(P, DUAL ? K_DUAL : K_PRIMAL);
 }
 
+// Direct variant (SliceGeo.stages == 0): only the sub-slice and the item's
+// row pointers are staged; the streamed rows and the CSR are read from global
+// memory by 1024 threads (32 warps per SM, the register-gather kernels'
+// occupancy). A row then costs one L2 round trip per batch of 4 nonzeros
+// (ci/cv; the operand rows come from shared memory) instead of two.
+constexpr int kSliceDirectThreads = 1024;
+
+template <bool DUAL>
+__global__ void __launch_bounds__(kSliceDirectThreads, 1) k_slice_direct(Params P) {
+  constexpr int W = 32;
+  constexpr int NS = DUAL ? 3 : 2;
+  extern __shared__ __align__(128) char slice_smem[];
+  __shared__ double red[(kSliceDirectThreads / 32) * NS * kSliceCols];
+  __shared__ SColInfo scol[kSliceCols];
+  const Ctrl C = *P.ctrl;
+  if (C.done) return;
+  prof_begin(P, DUAL ? K_DUAL : K_PRIMAL);
+  const int rows = DUAL ? P.m : P.n, rows_in = DUAL ? P.n : P.m;
+  const int* __restrict__ rp = DUAL ? P.rp : P.trp;
+  const int* __restrict__ ci = DUAL ? P.ci : P.tci;
+  const double* __restrict__ cv = DUAL ? P.cv : P.tcv;
+  const int tid = threadIdx.x, g = tid / kSliceLanes, li = tid - g * kSliceLanes;
+  const int groups = blockDim.x / kSliceLanes;
+  double* sl = reinterpret_cast<double*>(slice_smem);
+  int* rps = reinterpret_cast<int*>(slice_smem + slice_bytes(rows_in));
+  const int reset = C.anchor_reset;
+  const double alpha = C.alpha, oma = 1.0 - alpha;
+  const int cur = C.cur;
+  const double* gsrc = DUAL ? P.XT : P.Y[cur];
+  const int nvb = (C.active + kSliceCols - 1) / kSliceCols;
+  const int R = slice_items(rows, nvb, gridDim.x);
+  const int items = nvb * R;
+  const int per = (rows + R - 1) / R;
+  for (int w = blockIdx.x; w < items; w += gridDim.x) {
+    const int vb = w / R, r = w - vb * R;
+    const int b = vb >> 2, q = vb & 3;
+    const int r0 = min(rows, r * per), r1 = min(rows, r0 + per);
+    slice_rows(sl, gsrc, b, q, rows_in, 0, rows_in);
+    for (int t = tid; t <= r1 - r0; t += blockDim.x) rps[t] = __ldg(rp + r0 + t);
+    if (tid < kSliceCols) stage_col(P, b * W + q * kSliceCols + tid, C.active, DUAL, &scol[tid]);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    double acc[NS][2];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc[s][0] = acc[s][1] = 0.0;
+    const double* slo = sl + li * 2;
+    for (int i = r0 + g; i < r1; i += groups) {
+      const size_t idx = ((size_t)b * rows + i) * W + q * kSliceCols + li * 2;
+      // streamed operands and bounds first: their latency overlaps the gather
+      double2 s0, s1, s2 = make_double2(0.0, 0.0), s3 = make_double2(0.0, 0.0);
+      double bc = 0.0, lo, hi;
+      if constexpr (DUAL) {
+        lo = __ldg(P.rl + i);
+        hi = __ldg(P.ru + i);
+        s0 = __ldcs(reinterpret_cast<const double2*>(P.Y[cur] + idx));
+        s1 = __ldcs(reinterpret_cast<const double2*>(P.AX[cur] + idx));
+        if (!reset) {
+          s2 = __ldcs(reinterpret_cast<const double2*>(P.aY + idx));
+          s3 = __ldcs(reinterpret_cast<const double2*>(P.aAX + idx));
+        }
+      } else {
+        if (P.mode == BL_SHARED_OBJECTIVE) bc = __ldg(P.c + i);
+        lo = __ldg(P.xl + i);
+        hi = __ldg(P.xu + i);
+        s0 = __ldcs(reinterpret_cast<const double2*>(P.X[cur] + idx));
+        if (!reset) s1 = __ldcs(reinterpret_cast<const double2*>(P.aX + idx));
+      }
+      // one CSR row times this lane's two slots: stored order, separately
+      // rounded (csr_apply, sparse.hpp:176-183)
+      double gs[2] = {0.0, 0.0};
+      {
+        int p = rps[i - r0];
+        const int e = rps[i - r0 + 1];
+        for (; p < e; p += 4) {
+          int c[4];
+          double a[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const bool in = p + k < e;
+            c[k] = in ? __ldg(ci + p + k) : 0;
+            a[k] = in ? __ldg(cv + p + k) : 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (p + k < e) {
+              const double2 x = *reinterpret_cast<const double2*>(slo + (size_t)c[k] * kSliceCols);
+              gs[0] = __dadd_rn(gs[0], __dmul_rn(a[k], x.x));
+              gs[1] = __dadd_rn(gs[1], __dmul_rn(a[k], x.y));
+            }
+          }
+        }
+      }
+      if constexpr (DUAL) {
+        const double y[2] = {s0.x, s0.y}, ax[2] = {s1.x, s1.y};
+        const double ay[2] = {reset ? y[0] : s2.x, reset ? y[1] : s2.y};
+        const double aax[2] = {reset ? ax[0] : s3.x, reset ? ax[1] : s3.y};
+        double yn[2], axn[2];
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const ColInfo cl = read_col(&scol[li * 2 + v]);
+          const double sigma = cl.step;
+          // dual_step_element, solver.hpp:186-190
+          const double vv = 2.0 * gs[v] - ax[v];
+          const double sv = y[v] / sigma + vv;
+          const double yt = sigma * (sv - project_box(sv, lo, hi));
+          const double dy = yt - y[v];
+          const double da = y[v] - ay[v];
+          if (cl.valid) {
+            acc[0][v] += dy * dy;
+            acc[1][v] += dy * (gs[v] - ax[v]);
+            acc[NS - 1][v] += da * da;
+          }
+          yn[v] = alpha * (2.0 * yt - y[v]) + oma * ay[v];
+          axn[v] = alpha * (2.0 * gs[v] - ax[v]) + oma * aax[v];
+        }
+        __stcs(reinterpret_cast<double2*>(P.Y[cur ^ 1] + idx), make_double2(yn[0], yn[1]));
+        __stcs(reinterpret_cast<double2*>(P.AX[cur ^ 1] + idx), make_double2(axn[0], axn[1]));
+        if (reset) {
+          __stcs(reinterpret_cast<double2*>(P.aY + idx), s0);
+          __stcs(reinterpret_cast<double2*>(P.aAX + idx), s1);
+        }
+      } else {
+        const double x[2] = {s0.x, s0.y};
+        const double ax[2] = {reset ? x[0] : s1.x, reset ? x[1] : s1.y};
+        double xt[2], xn[2];
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const ColInfo cl = read_col(&scol[li * 2 + v]);
+          double cc, l2, h2;
+          col_vals(P, cl, i, bc, lo, hi, cc, l2, h2);
+          const double t = cc + gs[v];
+          xt[v] = project_box(x[v] - cl.step * t, l2, h2);
+          const double dx = xt[v] - x[v];
+          const double da = x[v] - ax[v];
+          if (cl.valid) {
+            acc[0][v] += dx * dx;
+            acc[1][v] += da * da;
+          }
+          xn[v] = alpha * (2.0 * xt[v] - x[v]) + oma * ax[v];
+        }
+        *reinterpret_cast<double2*>(P.XT + idx) = make_double2(xt[0], xt[1]);
+        __stcs(reinterpret_cast<double2*>(P.X[cur ^ 1] + idx), make_double2(xn[0], xn[1]));
+        if (reset) __stcs(reinterpret_cast<double2*>(P.aX + idx), s0);
+      }
+    }
+    slice_publish<NS>(acc, vb, r, R, P.slice_part, P.slice_cnt, P.colsum, DUAL ? S_DY2 : S_DX2,
+                      P.Kp, red);
+  }
+  prof_end(P, DUAL ? K_DUAL : K_PRIMAL);
+}
+
 }  // namespace bl

@@ -321,7 +321,21 @@ bool tile_map(CUtensorMap* m, const double* base, size_t rows, unsigned box_cols
 // gathers from `rows_in` rows, streaming `na` arrays: the largest chunk that
 // leaves >= 3 pipeline stages in shared memory (else >= 2), the nonzero
 // capacity of any chunk-sized row window (bl_slice.cuh).
-bool slice_geometry(int na, int rows, int rows_in, const std::vector<int>& h, bl::SliceGeo* g) {
+// BATCHLP_SLICE: 0 = register-gather kernels (default), 1 = staged slice
+// kernels, 2 = direct slice kernels.
+int slice_mode() {
+  const char* e = std::getenv("BATCHLP_SLICE");
+  return e ? std::atoi(e) : 0;
+}
+
+bool slice_geometry(bool direct, int na, int rows, int rows_in, const std::vector<int>& h,
+                    bl::SliceGeo* g) {
+  if (direct) {  // sub-slice + row pointers only (stages = 0)
+    const int bytes = bl::slice_bytes(rows_in) + bl::slice_rp_bytes(rows);
+    if (bytes > 227 * 1024 - 8192) return false;
+    *g = bl::SliceGeo{1, 0, 0, bytes};
+    return true;
+  }
   constexpr int kMaxDyn = 227 * 1024 - 6144;  // minus the kernels' static shared memory
   const int avail = kMaxDyn - bl::slice_bytes(rows_in) - bl::slice_rp_bytes(rows);
   if (avail <= 0 || (int)h.size() != rows + 1) return false;
@@ -828,9 +842,9 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.slice_cnt = nullptr;
   P.slice_p = P.slice_d = bl::SliceGeo{0, 0, 0, 0};
   if (W == 32 && !P.tma_host && m <= bl::kSliceMaxRows && n <= bl::kSliceMaxRows && m > 0 &&
-      n > 0 && std::getenv("BATCHLP_SLICE") && std::getenv("BATCHLP_SLICE")[0] == '1' &&
-      slice_geometry(2, n, m, p->h_trp, &P.slice_p) &&
-      slice_geometry(4, m, n, p->h_rp, &P.slice_d)) {
+      n > 0 && slice_mode() > 0 &&
+      slice_geometry(slice_mode() == 2, 2, n, m, p->h_trp, &P.slice_p) &&
+      slice_geometry(slice_mode() == 2, 4, m, n, p->h_rp, &P.slice_d)) {
     const int nvb = Kp / bl::kSliceCols;
     P.slice_part = static_cast<double*>(ctx->buf[bl_ctx::B_SPART].ensure(
         sizeof(double) * (size_t)nvb * bl::kSliceRMax * 3 * bl::kSliceCols));

@@ -149,14 +149,14 @@ def test_tma_gather_kernels_agree_with_reference_c2_prefix(ref, monkeypatch):
             assert abs(g.objective - w.objective) <= 1e-6 * (1 + abs(w.objective))
 
 
-@pytest.mark.parametrize("geometry", ["auto", "128/2", "64/4", "32/2"])
+@pytest.mark.parametrize("geometry", ["direct", "auto", "128/2", "64/4", "32/2"])
 def test_slice_kernels_agree_with_reference_c2_prefix(ref, geometry, monkeypatch):
-    """The slice-staged kernels (bl_slice.cuh: 8-slot operand sub-slice in
-    shared memory, TMA-pipelined row chunks) at several chunk / stage
-    geometries: C2 OBBT capped at 256 iterations matches the reference."""
+    """The slice kernels (bl_slice.cuh: 8-slot operand sub-slice in shared
+    memory; direct, or with pipelined row chunks at several chunk / stage
+    geometries): C2 OBBT capped at 256 iterations matches the reference."""
     monkeypatch.setenv("BATCHLP_LOOP", "graph")
-    monkeypatch.setenv("BATCHLP_SLICE", "1")
-    if geometry != "auto":
+    monkeypatch.setenv("BATCHLP_SLICE", "2" if geometry == "direct" else "1")
+    if geometry not in ("auto", "direct"):
         ch, st = geometry.split("/")
         monkeypatch.setenv("BATCHLP_SLICE_CH", ch)
         monkeypatch.setenv("BATCHLP_SLICE_STAGES", st)
