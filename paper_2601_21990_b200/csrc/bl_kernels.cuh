@@ -1778,7 +1778,17 @@ struct TailRows {
   const int *prp, *pci, *drp, *dci;
   const double *pcv, *dcv;
   int epoch;
+  // in-kernel profile of the fast passes (CTA 0, thread 0): phase start and
+  // [primal, dual, decide] x [ns, passes, algorithmic bytes], flushed to
+  // P.prof_acc once at exit instead of per-pass global stamps and atomics
+  int prof_on;
+  unsigned long long pt;
+  double pacc[3][3];
 };
+static __device__ __noinline__ double* tail_w() {
+  __shared__ double w[32];  // slot weights (staged with the column descriptors)
+  return w;
+}
 static __device__ __noinline__ SColInfo* tail_cols(int which) {
   __shared__ SColInfo s[2][32];  // [0] primal steps (tau), [1] dual steps (sigma)
   return s[which];
@@ -1796,6 +1806,19 @@ __device__ __forceinline__ void tail_mark(const Params& P, int k) {
     if (k > 0) P.dbg[k] += now - t->mark;
     else P.dbg[0] += 1;
     t->mark = now;
+  }
+}
+
+// Closes fast-pass phase k (0 primal, 1 dual, 2 decide) on CTA 0.
+__device__ __forceinline__ void tail_phase(int k) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    TailRows* t = tail_rows();
+    if (t->prof_on) {
+      const unsigned long long now = gtime();
+      t->pacc[k][0] += (double)(now - t->pt);
+      t->pacc[k][1] += 1.0;
+      t->pt = now;
+    }
   }
 }
 
@@ -1937,7 +1960,6 @@ static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* re
   const int tid = threadIdx.x, g = tid / L, li = tid - g * L;
   const bool tiny_n = P.n <= kTinyRows, tiny_m = P.m <= kTinyRows;
   {
-    prof_begin(P, K_PRIMAL);
     PrimalOp<W, false, true> op(P, C);
     op.col = tail_cols(0) + li * V;
     op.crp = t->prp;
@@ -1958,13 +1980,12 @@ static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* re
     }
     tail_mark(P, 2);
     tail_publish<W, 2, LL, NT>(P, acc, 0, red);
-    prof_end(P, K_PRIMAL);
     tail_mark(P, 3);
   }
   cluster_sync_all();
+  tail_phase(0);
   tail_mark(P, 4);
   {
-    prof_begin(P, K_DUAL);
     DualOp<W, false, false, true> op(P, C);
     op.col = tail_cols(1) + li * V;
     op.crp = t->drp;
@@ -1985,10 +2006,10 @@ static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* re
     }
     tail_mark(P, 5);
     tail_publish<W, 3, LL, NT>(P, acc, 2, red);
-    prof_end(P, K_DUAL);
     tail_mark(P, 6);
   }
   cluster_sync_all();
+  tail_phase(1);
   tail_mark(P, 7);
 }
 
@@ -1998,13 +2019,6 @@ static __device__ void tail_decide(const Params& P) {
   const int lane = threadIdx.x;
   Ctrl& C = *tail_ctrl();
   if (lane == 0) C = *tail_ctrl_in();
-  __syncwarp();
-  {
-    unsigned long long now = 0;
-    if (lane == 0) now = gtime();
-    now = __shfl_sync(0xffffffffu, now, 0);
-    prof_fold(P, C, lane, now);
-  }
   __syncwarp();
   const int active = C.active;
   const int cl = gridDim.x;
@@ -2025,7 +2039,7 @@ static __device__ void tail_decide(const Params& P) {
     csr(P, S_DY2, lane) = dy2;
     csr(P, S_CROSS, lane) = cross;
     csr(P, S_YA2, lane) = ya2;
-    w = P.w[lane];
+    w = tail_w()[lane];
     r = m_residual(dx2, dy2, cross, P.eta, w, &err);
     P.resid[lane] = r;
   }
@@ -2040,16 +2054,21 @@ static __device__ void tail_decide(const Params& P) {
   if (bad || loop_err) {
     if (lane == 0) {
       C.error = loop_err ? BL_ERR_LOGIC : BL_ERR_DOMAIN;
-      if (P.prof) atomicMax(&P.prof[2 * K_DECIDE + 1], gtime());
       C.done = 1;
       *P.ctrl = C;
     }
     tail_broadcast_ctrl(lane);
     return;
   }
-  // averaged residual: sequential sum in slot order (ordered_sum, count <= 256)
+  // averaged residual: sequential sum in slot order (ordered_sum, count <= 256);
+  // the terms are staged in shared memory so their loads issue back to back
+  __shared__ double rs[32];
+  rs[lane] = r;
+  __syncwarp();
   double sum = 0.0;
-  for (int j = 0; j < active; ++j) sum += __shfl_sync(0xffffffffu, r, j);
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j < active) sum += rs[j];
   const double mean = sum / (double)active;
   const bool first = C.inner_k == 0;
   if (first && lane < active) P.anchor_resid[lane] = r;
@@ -2103,7 +2122,6 @@ static __device__ void tail_decide(const Params& P) {
     C.check = (C.total_k % P.period == 0) || C.at_cap;
     C.cert_pending = 0;
     *P.ctrl = C;
-    if (P.prof) atomicMax(&P.prof[2 * K_DECIDE + 1], gtime());
   }
   tail_broadcast_ctrl(lane);
 }
@@ -2118,9 +2136,16 @@ static __device__ void tail_pass(const Params& P, const Ctrl& C, double* red) {
       stage_col(P, tid, C.active, false, tail_cols(0) + tid);
       stage_col(P, tid, C.active, true, tail_cols(1) + tid);
     }
+    if (tid < 32) tail_w()[tid] = tid < C.active ? P.w[tid] : 1.0;
     __syncthreads();
     if (tid == 0) t->epoch = C.col_epoch;
     __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && t->prof_on) {
+    // algorithmic bytes of the pass (prof_fold's model, plain pass)
+    const double n = P.n, m = P.m, nnz = (double)P.nnz, K = C.active;
+    t->pacc[0][2] += 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 4.0 * n);
+    t->pacc[1][2] += 12.0 * nnz + 4.0 * (m + 1) + 16.0 * m + 8.0 * K * (n + 6.0 * m);
   }
   const int Lsel = pass_lanes<W>(C.active);
   tail_mark(P, 1);
@@ -2128,6 +2153,7 @@ static __device__ void tail_pass(const Params& P, const Ctrl& C, double* red) {
   if (blockIdx.x == 0 && threadIdx.x < 32) tail_decide(P);
   tail_mark(P, 8);
   cluster_sync_all();
+  tail_phase(2);
   tail_mark(P, 9);
 }
 
@@ -2151,11 +2177,33 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail_fast(Params P, int tai
   tail_setup(P, tail_dyn, tail_smem);
   if (threadIdx.x == 0) *tail_ctrl_in() = load_ctrl(P.ctrl);
   __syncthreads();
+  // Profiling: fold the stamps a generic pass left (CTA 0), then time the
+  // fast passes locally (tail_phase); the fast passes write no global stamps.
+  TailRows* tr = tail_rows();
+  if (threadIdx.x == 0) {
+    tr->prof_on = blockIdx.x == 0 && P.prof != nullptr;
+    for (int k = 0; k < 3; ++k) tr->pacc[k][0] = tr->pacc[k][1] = tr->pacc[k][2] = 0.0;
+  }
+  __syncthreads();
+  if (tr->prof_on && threadIdx.x < 32) {
+    const Ctrl C0 = *tail_ctrl_in();
+    prof_fold(P, C0, threadIdx.x, gtime());
+  }
+  __syncthreads();
   for (;;) {
     tail_mark(P, 0);
     const Ctrl C = *tail_ctrl_in();
     if (C.done || !tail_fast_ok(P, C, W)) break;
+    if (tr->prof_on && threadIdx.x == 0) tr->pt = gtime();
     tail_pass<W, kTailThreads>(P, C, red);
+  }
+  if (tr->prof_on && threadIdx.x == 0) {
+    const int kinds[3] = {K_PRIMAL, K_DUAL, K_DECIDE};
+    for (int k = 0; k < 3; ++k)
+      for (int f = 0; f < 3; ++f) P.prof_acc[3 * kinds[k] + f] += tr->pacc[k][f];
+    // the next generic decide starts a fresh decide interval
+    P.prof[2 * K_DECIDE] = ~0ull;
+    P.prof[2 * K_DECIDE + 1] = 0ull;
   }
 }
 
