@@ -13,8 +13,9 @@ iteration loop, one all_gather of per-LP scalars at the end); value = all LPs
 
   value     device-resident solve: problem already in HBM, time from CUDA
             events recorded on the solver's own stream (max over ranks)
-  e2e       the public API from pinned host arrays: problem upload, step size,
-            solve and per-LP result read-back inside the timed region
+  e2e       the drop-in C-ABI (bl_problem_assign + bl_solve_batch, what the
+            C++ headers call) from pinned host arrays: problem upload, step
+            size, solve and per-LP result read-back inside the timed region
   roofline  dominant kernel (in-situ %globaltimer spans inside the graph)
             algorithmic bytes / time vs MEASURED_PEAKS.json hbm_gbs
   cpu_baseline  the reference CPU path (oracle/_ref) on a bounded sample
@@ -285,19 +286,47 @@ def main():
     per_solve_h2d = n_ov * 24 + my_batch.batch_width() * (8 * 19 + 4 * 7 + 4 * 3) + 256
     per_solve_d2h = my_batch.batch_width() * (80 + 4) + 256
     # One long-lived workspace, as a solver process keeps its device context;
-    # every step still uploads the problem from pinned host memory, recomputes
-    # the step size (device power iteration) and reads the per-LP results back.
+    # every step uploads the problem from pinned host memory into it
+    # (bl_problem_assign), recomputes the step size (device power iteration)
+    # and reads the per-LP results back into a host array (bl_solve_batch):
+    # the calls the C++ drop-in headers make.
+    import ctypes
+    from paper_2601_21990_b200 import _native as NN
     e2e_walls = []
     wse = BatchWorkspace(local)
-    s = bl.solve_batch(e2e_batch, cfg, my_presets, wse, vectors=bl.Vectors.NONE,
-                       cache_problem=False)  # warm-up
+    dpe = wse.resident(e2e_prob, cache=False)  # device problem (warm-up upload)
+    Lb = NN.lib()
+    _, _, assign_args, keep = type(dpe)._arrays(e2e_prob)
+    ovs = my_batch.overrides()
+    ov_arr = (NN.bl_override * max(len(ovs), 1))()
+    for k, o in enumerate(ovs):
+        ov_arr[k].column, ov_arr[k].kind = o.column, int(o.kind)
+        ov_arr[k].variable, ov_arr[k].value = o.variable, o.value
+    pcols = np.array([q.column for q in my_presets], dtype=np.int32)
+    ccfg = cfg.to_c(bl.Vectors.NONE, 0.0)
+    summ = NN.bl_summary()
+    res_h = (NN.bl_column_result * max(my_batch.batch_width(), 1))()
+
+    def c_abi_solve():
+        rc = Lb.bl_problem_assign(wse.ctx.handle, dpe.handle, *assign_args)
+        if rc == 0:
+            rc = Lb.bl_solve_batch(wse.ctx.handle, dpe.handle, my_batch.batch_width(),
+                                   int(my_batch.objective_mode()), ov_arr, len(ovs),
+                                   ctypes.byref(ccfg), NN.iptr(pcols) if len(pcols) else None,
+                                   len(pcols), None, None, None, ctypes.byref(summ), res_h)
+        if rc != 0:
+            raise RuntimeError(f"bl_solve_batch failed: {rc} {Lb.bl_last_error(wse.ctx.handle)}")
+
+    c_abi_solve()  # warm-up
     for _ in range(args.steps):
         flush_l2(torch, dev)
         barrier()
         t0 = time.perf_counter()
-        s = bl.solve_batch(e2e_batch, cfg, my_presets, wse, vectors=bl.Vectors.NONE,
-                           cache_problem=False)
+        c_abi_solve()
         e2e_walls.append(time.perf_counter() - t0)
+    if summ.iterations != s.iterations:
+        raise RuntimeError("e2e solve disagrees with the device-resident solve")
+    del keep
     wse.ctx.close()
     e2e_s = sum(e2e_walls) / len(e2e_walls)
     if world > 1:
@@ -342,6 +371,18 @@ def main():
                 "alg_bytes_per_launch": round(row[dom][2] / row[dom][0]),
                 "avg_launch_us": round(row[dom][1] / row[dom][0] / 1e3, 3),
                 "share_of_kernel_time": round(row[dom][1] / total_ns, 3) if total_ns else None,
+                # the fast tail kernel (k_tail_fast: <= 32 LPs left, one
+                # 16-CTA cluster) is latency-bound by construction; its
+                # phases are timed on chip per pass
+                "tail_kernel": ({
+                    "kernel": "k_tail_fast", "bound": "latency",
+                    "passes": int(prof["tail_decide"][0]),
+                    "us_per_pass": round(sum(prof[k][1] for k in ("tail_primal", "tail_dual",
+                                                                  "tail_decide"))
+                                         / prof["tail_decide"][0] / 1e3, 3),
+                    "share_of_kernel_time": round(sum(prof[k][1] for k in (
+                        "tail_primal", "tail_dual", "tail_decide")) / total_ns, 3)}
+                    if prof.get("tail_decide", [0])[0] else None),
                 "kernels": {k: {"launches": int(v[0]), "ms": round(v[1] / 1e6, 3),
                                 "GB/s": round(v[2] / v[1], 1) if v[1] and v[2] else None}
                             for k, v in sorted(prof.items()) if v[0]}}

@@ -1782,9 +1782,21 @@ struct TailRows {
   // [primal, dual, decide] x [ns, passes, algorithmic bytes], flushed to
   // P.prof_acc once at exit instead of per-pass global stamps and atomics
   int prof_on;
+  int npass;  // fast passes run by this launch
   unsigned long long pt;
   double pacc[3][3];
 };
+// Per-slot state of the fast decide kept in CTA 0's shared memory during the
+// launch and written back at exit: the five column sums and the residual of
+// the last pass ([6][32]), and the anchor residuals.
+static __device__ __noinline__ double* tail_sums() {
+  __shared__ double t[6 * 32];
+  return t;
+}
+static __device__ __noinline__ double* tail_ar() {
+  __shared__ double t[32];
+  return t;
+}
 static __device__ __noinline__ double* tail_w() {
   __shared__ double w[32];  // slot weights (staged with the column descriptors)
   return w;
@@ -2018,6 +2030,8 @@ static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* re
 static __device__ void tail_decide(const Params& P) {
   const int lane = threadIdx.x;
   Ctrl& C = *tail_ctrl();
+  unsigned long long tdbg = 0;
+  if (P.dbg && lane == 0) tdbg = gtime();
   if (lane == 0) C = *tail_ctrl_in();
   __syncwarp();
   const int active = C.active;
@@ -2034,16 +2048,22 @@ static __device__ void tail_decide(const Params& P) {
       cross = __dadd_rn(cross, tp[96]);
       ya2 = __dadd_rn(ya2, tp[128]);
     }
-    csr(P, S_DX2, lane) = dx2;
-    csr(P, S_XA2, lane) = xa2;
-    csr(P, S_DY2, lane) = dy2;
-    csr(P, S_CROSS, lane) = cross;
-    csr(P, S_YA2, lane) = ya2;
+    double* ts = tail_sums();
+    ts[0 * 32 + lane] = dx2;
+    ts[1 * 32 + lane] = xa2;
+    ts[2 * 32 + lane] = dy2;
+    ts[3 * 32 + lane] = cross;
+    ts[4 * 32 + lane] = ya2;
     w = tail_w()[lane];
     r = m_residual(dx2, dy2, cross, P.eta, w, &err);
-    P.resid[lane] = r;
+    ts[5 * 32 + lane] = r;
   }
   const bool bad = __any_sync(0xffffffffu, err != 0);
+  if (P.dbg && lane == 0) {  // diagnostic split of the fast decide (BATCHLP_TAIL_TRACE)
+    const unsigned long long now = gtime();
+    P.dbg[14] += now - tdbg;
+    tdbg = now;
+  }
   int loop_err = 0;
   if (lane == 0) {
     C.launches += 3;
@@ -2055,7 +2075,6 @@ static __device__ void tail_decide(const Params& P) {
     if (lane == 0) {
       C.error = loop_err ? BL_ERR_LOGIC : BL_ERR_DOMAIN;
       C.done = 1;
-      *P.ctrl = C;
     }
     tail_broadcast_ctrl(lane);
     return;
@@ -2071,7 +2090,7 @@ static __device__ void tail_decide(const Params& P) {
     if (j < active) sum += rs[j];
   const double mean = sum / (double)active;
   const bool first = C.inner_k == 0;
-  if (first && lane < active) P.anchor_resid[lane] = r;
+  if (first && lane < active) tail_ar()[lane] = r;
   // restart rule (solver.hpp:299-311) on the pre-step state
   int reason = -1;
   if (C.inner_k >= 1) {
@@ -2082,10 +2101,11 @@ static __device__ void tail_decide(const Params& P) {
       reason = BL_RESTART_ARTIFICIAL;
   }
   if (reason >= 0 && lane < active) {
-    const double ar = first ? r : P.anchor_resid[lane];
+    const double ar = first ? r : tail_ar()[lane];
     if (r <= ar) P.w[lane] = smoothed_weight(w, sqrt(xa2), sqrt(ya2), P.theta);
   }
   __syncwarp();  // every lane has read the control block
+  if (P.dbg && lane == 0) P.dbg[15] += gtime() - tdbg;
   if (lane == 0) {
     if (first) C.mean_anchor = mean;
     C.mean = mean;
@@ -2121,7 +2141,6 @@ static __device__ void tail_decide(const Params& P) {
     C.at_cap = C.total_k >= P.max_it;
     C.check = (C.total_k % P.period == 0) || C.at_cap;
     C.cert_pending = 0;
-    *P.ctrl = C;
   }
   tail_broadcast_ctrl(lane);
 }
@@ -2189,6 +2208,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail_fast(Params P, int tai
     const Ctrl C0 = *tail_ctrl_in();
     prof_fold(P, C0, threadIdx.x, gtime());
   }
+  if (blockIdx.x == 0 && threadIdx.x < W) tail_ar()[threadIdx.x] = P.anchor_resid[threadIdx.x];
+  if (threadIdx.x == 0) tr->npass = 0;
   __syncthreads();
   for (;;) {
     tail_mark(P, 0);
@@ -2196,9 +2217,28 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail_fast(Params P, int tai
     if (C.done || !tail_fast_ok(P, C, W)) break;
     if (tr->prof_on && threadIdx.x == 0) tr->pt = gtime();
     tail_pass<W, kTailThreads>(P, C, red);
+    if (threadIdx.x == 0) tr->npass += 1;
+  }
+  // write back the decide state the fast passes kept on chip (CTA 0)
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const Ctrl& C = *tail_ctrl_in();
+    if (tr->npass > 0) {
+      if (lane < W) P.anchor_resid[lane] = tail_ar()[lane];
+      if (lane < C.active) {
+        const double* ts = tail_sums();
+        csr(P, S_DX2, lane) = ts[0 * 32 + lane];
+        csr(P, S_XA2, lane) = ts[1 * 32 + lane];
+        csr(P, S_DY2, lane) = ts[2 * 32 + lane];
+        csr(P, S_CROSS, lane) = ts[3 * 32 + lane];
+        csr(P, S_YA2, lane) = ts[4 * 32 + lane];
+        P.resid[lane] = ts[5 * 32 + lane];
+      }
+      if (lane == 0) *P.ctrl = C;
+    }
   }
   if (tr->prof_on && threadIdx.x == 0) {
-    const int kinds[3] = {K_PRIMAL, K_DUAL, K_DECIDE};
+    const int kinds[3] = {K_TAIL_PRIMAL, K_TAIL_DUAL, K_TAIL_DECIDE};
     for (int k = 0; k < 3; ++k)
       for (int f = 0; f < 3; ++f) P.prof_acc[3 * kinds[k] + f] += tr->pacc[k][f];
     // the next generic decide starts a fresh decide interval

@@ -979,6 +979,8 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
     std::fprintf(stderr, "[decide trace] %llu plain passes\n", (unsigned long long)d[10]);
     for (int k = 11; k < 14; ++k)
       std::fprintf(stderr, "[decide trace] %-16s %8.3f us/pass\n", dwhat[k - 11], d[k] / dp / 1e3);
+    std::fprintf(stderr, "[fast decide] ctrl+fold+resid %8.3f us/pass\n", d[14] / passes / 1e3);
+    std::fprintf(stderr, "[fast decide] mean+rule       %8.3f us/pass\n", d[15] / passes / 1e3);
   }
   const bl::Ctrl C = *ctx->h_ctrl;
   if (C.error == BL_ERR_DOMAIN)
@@ -1000,8 +1002,10 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   sum.kernel_launches = C.launches + 2;  // + init and AX = A X
   sum.loop_passes = C.passes;
   {
-    static const char* names[bl::K_KINDS] = {"primal", "dual", "check", "decide",
-                                             "cert", "snapshot", "compact", "trace"};
+    static const char* names[bl::K_KINDS] = {"primal",      "dual",      "check",
+                                             "decide",      "cert",      "snapshot",
+                                             "compact",     "trace",     "tail_primal",
+                                             "tail_dual",   "tail_decide"};
     ctx->last_prof.assign(bl::K_KINDS, bl_kernel_stat{});
     for (int k = 0; k < bl::K_KINDS; ++k) {
       bl_kernel_stat& st = ctx->last_prof[k];

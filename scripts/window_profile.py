@@ -38,7 +38,8 @@ for cap in caps:
     done = sum(1 for r in cur.per_problem if int(r.status) != 3)
     line = f"  ..{cap:6d}: {passes:6d} passes {ms:9.2f} ms {1e3 * ms / max(passes, 1):8.2f} us/pass finished={done}"
     parts = []
-    for k in ("primal", "dual", "decide", "check", "cert", "compact", "snapshot"):
+    for k in ("primal", "dual", "decide", "check", "cert", "compact", "snapshot",
+              "tail_primal", "tail_dual", "tail_decide"):
         lf, nf, _ = cur.profile.get(k, (0, 0, 0))
         lp, np_, _ = prev.profile.get(k, (0, 0, 0)) if prev else (0, 0, 0)
         if lf - lp > 0:
