@@ -2188,12 +2188,19 @@ __device__ __forceinline__ bool tail_fast_ok(const Params& P, const Ctrl& C, int
 // kernel then runs that one pass (single-pass mode) and the tail graph loops
 // (bl_solver.cu). More threads per CTA than the generic kernel: more row
 // groups, so fewer rows per group in a pass.
-constexpr int kTailThreads = 512;
+// (threads per CTA of the fast tail kernel; its reduction scratch is
+// kTailRedBytes of dynamic shared memory)
+#ifndef BL_TAIL_THREADS
+#define BL_TAIL_THREADS 512
+#endif
+constexpr int kTailThreads = BL_TAIL_THREADS;
+constexpr int kTailRedBytes = (kTailThreads / 32) * 3 * 32 * 8;
 template <int W>
 __global__ void __launch_bounds__(kTailThreads, 1) k_tail_fast(Params P, int tail_smem) {
-  __shared__ double red[(kTailThreads / 32) * 3 * 32];
+  // dynamic shared memory: the per-warp reduction scratch, then the CSR cache
   extern __shared__ __align__(16) char tail_dyn[];
-  tail_setup(P, tail_dyn, tail_smem);
+  double* red = reinterpret_cast<double*>(tail_dyn);
+  tail_setup(P, tail_dyn + kTailRedBytes, tail_smem);
   if (threadIdx.x == 0) *tail_ctrl_in() = load_ctrl(P.ctrl);
   __syncthreads();
   // Profiling: fold the stamps a generic pass left (CTA 0), then time the
@@ -2556,14 +2563,13 @@ cudaError_t WLaunch<W>::tail_fast(const Params& P, cudaStream_t s, int tail_smem
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
-  if (tail_smem > 0) {
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tail_smem);
-    if (e != cudaSuccess) return e;
-  }
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           tail_smem + kTailRedBytes);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P.grid);
   cfg.blockDim = dim3(kTailThreads);
-  cfg.dynamicSmemBytes = tail_smem;
+  cfg.dynamicSmemBytes = tail_smem + kTailRedBytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
