@@ -203,6 +203,14 @@ int bl_spectral_norm(bl_ctx* ctx, bl_problem* p, double* out);
  * to the reference csr_apply (sparse.hpp:176-183). */
 int bl_spmm(bl_ctx* ctx, const bl_problem* p, int transpose, int32_t width,
             int32_t active, const double* x, double* out);
+/* measure_spmm (tuner.hpp:72-108) on the device: `repetitions` products
+ * A X and `repetitions` products A'Y of `width` columns (seeded blocks, two
+ * untimed warm-up rounds), timed with CUDA events on the context's stream;
+ * the cost of an empty event interval is subtracted and a clamp to zero is
+ * reported through *clamped. Seconds. BL_ERR_INVALID_ARGUMENT for width < 1
+ * or repetitions < 3, as the reference. */
+int bl_measure_spmm(bl_ctx* ctx, const bl_problem* p, int32_t width, int32_t repetitions,
+                    double* total_s, double* per_column_s, int32_t* clamped);
 
 /* ---- the hot path: solve_batch (batch_solver.hpp:78-355) -----------------
  * width LPs share A, the row bounds and (mode SHARED) the objective; each

@@ -17,4 +17,7 @@ from .drivers import (FsbBranch, FsbDriver, FsbOutcome, FsbRequest, ObbtConfig, 
                       ObbtVariable, build_fsb_batch, build_obbt_batch, certified_value,
                       run_fsb, run_obbt, score_branching)
 
+from .tuner import (TuneEntry, TuneReport, choose_width, default_tune_widths, measure_spmm,
+                    tune_batch_width, write_tune_csv)
+
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -105,6 +106,7 @@ struct bl_ctx {
     B_RC, B_R, B_DR, B_AXT, B_BX, B_BY, B_BR, B_RX, B_RY, B_RR, B_RDX, B_RDY, B_RDR,
     B_SLOTD, B_SLOTI, B_ORIGI, B_RES, B_COLSUM, B_PART, B_CNT, B_SNAP, B_MOVES,
     B_LOG, B_CTRL, B_PROF, B_PROFACC, B_BAR, B_OV, B_OVD, B_WARMX, B_WARMY, B_PI, B_TMP0, B_TMP1,
+    B_TUNE0, B_TUNE1, B_TUNE2, B_TUNE3,
     B_TAIL, B_DBG, B_SPART, B_SCNT, B_COUNT
   };
   DevBuf buf[B_COUNT];
@@ -1234,6 +1236,83 @@ int bl_spmm(bl_ctx* ctx, const bl_problem* p, int transpose, int32_t width,
     ck(cudaMemcpyAsync(out, raw, sizeof(double) * (size_t)rout * active, cudaMemcpyDeviceToHost, s), "out");
     ck(cudaStreamSynchronize(s), "spmm sync");
     ck(cudaGetLastError(), "spmm");
+  });
+}
+
+int bl_measure_spmm(bl_ctx* ctx, const bl_problem* p, int32_t width, int32_t repetitions,
+                    double* total_s, double* per_column_s, int32_t* clamped) {
+  return guarded(ctx, [&] {
+    if (width < 1) raise(BL_ERR_INVALID_ARGUMENT, "tuner: width must be >= 1");
+    if (repetitions < 3) raise(BL_ERR_INVALID_ARGUMENT, "tuner: need >= 3 repetitions");
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const int n = p->n, m = p->m;
+    // the reference's seeded blocks (tuner.hpp:79-82), column-major
+    std::mt19937_64 rng(0x5eedu);
+    std::vector<double> hx((size_t)n * width), hy((size_t)m * width);
+    for (double& v : hx) v = (double)(rng() >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+    for (double& v : hy) v = (double)(rng() >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+    const int W = pow2_width(width);
+    const int Kp = (width + W - 1) / W * W;
+    cudaStream_t s = ctx->stream;
+    auto dbuf = [&](int which, size_t rows) {
+      return static_cast<double*>(ctx->buf[which].ensure(sizeof(double) * (rows * Kp + 1)));
+    };
+    double* x = dbuf(bl_ctx::B_TUNE0, n);
+    double* y = dbuf(bl_ctx::B_TUNE1, m);
+    double* ax = dbuf(bl_ctx::B_TUNE2, m);
+    double* aty = dbuf(bl_ctx::B_TUNE3, n);
+    double* raw = static_cast<double*>(ctx->buf[bl_ctx::B_WARMX].ensure(
+        sizeof(double) * ((size_t)std::max(n, m) * width + 1)));
+    ck(cudaMemcpyAsync(raw, hx.data(), sizeof(double) * hx.size(), cudaMemcpyHostToDevice, s), "x");
+    bl::launch_to_tiled(s, raw, x, n, width, W, width);
+    ck(cudaMemcpyAsync(raw, hy.data(), sizeof(double) * hy.size(), cudaMemcpyHostToDevice, s), "y");
+    bl::launch_to_tiled(s, raw, y, m, width, W, width);
+    bl::Params P{};
+    P.m = m;
+    P.n = n;
+    P.rp = p->rp.as<int>();
+    P.ci = p->ci.as<int>();
+    P.cv = p->cv.as<double>();
+    P.trp = p->trp.as<int>();
+    P.tci = p->tci.as<int>();
+    P.tcv = p->tcv.as<double>();
+    P.W = W;
+    P.Kp = Kp;
+    P.grid = ctx->grid;
+    const int nb = Kp / W;
+    const int R = std::max(items_for(m, W, ctx->grid), items_for(n, W, ctx->grid));
+    P.partials = static_cast<double*>(
+        ctx->buf[bl_ctx::B_PART].ensure(sizeof(double) * (size_t)nb * R * 10 * W));
+    P.counters = static_cast<int*>(ctx->buf[bl_ctx::B_CNT].ensure(sizeof(int) * (size_t)std::max(nb, 64)));
+    ck(cudaMemsetAsync(P.counters, 0, sizeof(int) * (size_t)std::max(nb, 64), s), "counters");
+    P.colsum = static_cast<double*>(
+        ctx->buf[bl_ctx::B_COLSUM].ensure(sizeof(double) * bl::S_COUNT * (size_t)Kp));
+    for (int warm = 0; warm < 2; ++warm) {
+      bl::launch_spmm(P, s, false, x, ax, width);
+      bl::launch_spmm(P, s, true, y, aty, width);
+    }
+    ck(cudaEventRecord(ctx->ev0, s), "event");
+    for (int r = 0; r < repetitions; ++r) bl::launch_spmm(P, s, false, x, ax, width);
+    for (int r = 0; r < repetitions; ++r) bl::launch_spmm(P, s, true, y, aty, width);
+    ck(cudaEventRecord(ctx->ev1, s), "event");
+    ck(cudaEventSynchronize(ctx->ev1), "tuner sync");
+    ck(cudaGetLastError(), "tuner spmm");
+    float ms = 0.f, oms = 0.f;
+    ck(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "elapsed");
+    // the measurement's own overhead: an empty event interval
+    ck(cudaEventRecord(ctx->ev0, s), "event");
+    ck(cudaEventRecord(ctx->ev1, s), "event");
+    ck(cudaEventSynchronize(ctx->ev1), "tuner sync");
+    ck(cudaEventElapsedTime(&oms, ctx->ev0, ctx->ev1), "elapsed");
+    double total = ((double)ms - (double)oms) * 1e-3;
+    int cl = 0;
+    if (total < 0.0) {
+      total = 0.0;
+      cl = 1;
+    }
+    if (total_s) *total_s = total;
+    if (per_column_s) *per_column_s = total / width;
+    if (clamped) *clamped = cl;
   });
 }
 

@@ -156,6 +156,17 @@ inline int run_all(int argc, char** argv) {
     ::doctest::shim::report(doctest_shim_ok, "CHECK_THROWS_AS", #expr, __FILE__, __LINE__); \
   } while (0)
 
+#define CHECK_NOTHROW(...)                                                           \
+  do {                                                                               \
+    bool doctest_shim_ok = true;                                                     \
+    try {                                                                            \
+      static_cast<void>(__VA_ARGS__);                                                \
+    } catch (...) {                                                                  \
+      doctest_shim_ok = false;                                                       \
+    }                                                                                \
+    ::doctest::shim::report(doctest_shim_ok, "CHECK_NOTHROW", #__VA_ARGS__, __FILE__, __LINE__); \
+  } while (0)
+
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
 int main(int argc, char** argv) { return ::doctest::shim::run_all(argc, argv); }
 #endif

@@ -1,7 +1,7 @@
 """The C++ drop-in (include/batchlp/*.hpp over libbatchlp_cuda.so).
 
 * The reference's OWN unit suites (test_bounds, test_sparse, test_problem,
-  test_batch_solver, test_strong_branching, test_obbt), compiled unmodified
+  test_batch_solver, test_strong_branching, test_obbt, test_tuner), compiled unmodified
   against our headers by tests/cpp/Makefile, pass on the B200.
 * Our C++ API tests (tests/cpp/test_dropin.cpp) pass on the B200.
 * C1 strong branching and C2 OBBT through the C++ API match the reference's
