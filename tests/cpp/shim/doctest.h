@@ -48,6 +48,16 @@ class Approx {
   double scale_ = 1.0;
 };
 
+// doctest::Contains: a substring matcher for CHECK_THROWS_WITH_AS.
+class Contains {
+ public:
+  explicit Contains(const char* s) : s_(s) {}
+  bool matches(const char* what) const { return std::strstr(what, s_) != nullptr; }
+
+ private:
+  const char* s_;
+};
+
 namespace shim {
 
 struct Case {
@@ -165,6 +175,24 @@ inline int run_all(int argc, char** argv) {
       doctest_shim_ok = false;                                                       \
     }                                                                                \
     ::doctest::shim::report(doctest_shim_ok, "CHECK_NOTHROW", #__VA_ARGS__, __FILE__, __LINE__); \
+  } while (0)
+
+#define CHECK_THROWS_WITH_AS(expr, matcher, ...)                                     \
+  do {                                                                               \
+    bool doctest_shim_ok = false;                                                    \
+    try {                                                                            \
+      static_cast<void>(expr);                                                       \
+    } catch (const __VA_ARGS__& doctest_shim_e) {                                    \
+      doctest_shim_ok = (matcher).matches(doctest_shim_e.what());                    \
+    } catch (...) {                                                                  \
+    }                                                                                \
+    ::doctest::shim::report(doctest_shim_ok, "CHECK_THROWS_WITH_AS", #expr, __FILE__, __LINE__); \
+  } while (0)
+
+#define FAIL(msg)                                                                    \
+  do {                                                                               \
+    ::doctest::shim::report(false, "FAIL", msg, __FILE__, __LINE__);                 \
+    throw ::doctest::shim::Abort{};                                                  \
   } while (0)
 
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN

@@ -1,8 +1,11 @@
 """The C++ drop-in (include/batchlp/*.hpp over libbatchlp_cuda.so).
 
 * The reference's OWN unit suites (test_bounds, test_sparse, test_problem,
-  test_batch_solver, test_strong_branching, test_obbt, test_tuner), compiled unmodified
-  against our headers by tests/cpp/Makefile, pass on the B200.
+  test_batch_solver, test_strong_branching, test_obbt, test_tuner, test_mps,
+  test_generators), compiled unmodified against our headers by
+  tests/cpp/Makefile, pass on the B200 (test_mps / test_generators exercise
+  the reference's own host-side MPS reader and generators over our problem
+  types).
 * Our C++ API tests (tests/cpp/test_dropin.cpp) pass on the B200.
 * C1 strong branching and C2 OBBT through the C++ API match the reference's
   golden results (status identical, objective 1e-6 relative, iterations 10 %).
