@@ -152,7 +152,20 @@ __device__ __forceinline__ void gather_row(const int* __restrict__ rp,
     }
   }
   if constexpr (GENERIC) {  // the tail's cached rows: registers are scarce there
-    for (; p < e; ++p) {
+    if (p + 2 <= e) {  // a pair, loads issued together
+      const int c0 = ldi(ci + p), c1 = ldi(ci + p + 1);
+      const double a0 = ldd(cv + p), a1 = ldd(cv + p + 1);
+      double x0[V], x1[V];
+      ld_nc<V>(base + (size_t)c0 * W, x0);
+      ld_nc<V>(base + (size_t)c1 * W, x1);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        acc[v] = __dadd_rn(acc[v], __dmul_rn(a0, x0[v]));
+        acc[v] = __dadd_rn(acc[v], __dmul_rn(a1, x1[v]));
+      }
+      p += 2;
+    }
+    if (p < e) {
       const int c0 = ldi(ci + p);
       const double a0 = ldd(cv + p);
       double x0[V];
