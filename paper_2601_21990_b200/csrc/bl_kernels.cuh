@@ -133,6 +133,27 @@ __device__ __forceinline__ void gather_row(const int* __restrict__ rp,
   const int e = ldi(rp + i + 1);
 #pragma unroll
   for (int v = 0; v < V; ++v) acc[v] = 0.0;
+#ifndef BL_TAIL_GATHER8
+#define BL_TAIL_GATHER8 1
+#endif
+  if constexpr (GENERIC && BL_TAIL_GATHER8) {
+    // the tail's rows: 8 operand rows in flight per batch (latency-bound)
+    for (; p + 8 <= e; p += 8) {
+      int c[8];
+      double a[8], x[8][V];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        c[k] = ldi(ci + p + k);
+        a[k] = ldd(cv + p + k);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ld_nc<V>(base + (size_t)c[k] * W, x[k]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] = __dadd_rn(acc[v], __dmul_rn(a[k], x[k][v]));
+    }
+  }
   for (; p + 4 <= e; p += 4) {
     const int c0 = ldi(ci + p), c1 = ldi(ci + p + 1);
     const int c2 = ldi(ci + p + 2), c3 = ldi(ci + p + 3);
