@@ -1819,6 +1819,7 @@ struct TailRows {
   int npass;  // fast passes run by this launch
   unsigned long long pt;
   double pacc[3][3];
+  double* part;  // the double-buffered partials (dynamic shared memory)
 };
 // Per-slot state of the fast decide kept in CTA 0's shared memory during the
 // launch and written back at exit: the five column sums and the residual of
@@ -1868,11 +1869,14 @@ __device__ __forceinline__ void tail_phase(int k) {
   }
 }
 
-// [cluster CTA][5 sums][32 slots]: per-CTA partials of a fast tail pass,
-// written into CTA 0's copy through distributed shared memory.
-static __device__ __noinline__ double* tail_part_smem() {
-  __shared__ double t[16 * 5 * 32];
-  return t;
+// [pass parity][cluster CTA][5 sums][32 slots]: the partials of a fast tail
+// pass. Every CTA keeps a full copy in its dynamic shared memory; each CTA
+// pushes its own partials into all copies through distributed shared memory,
+// so every CTA can run the (deterministic) decide itself. Double-buffered by
+// pass parity: a CTA can be one phase ahead of another, never more.
+constexpr int kTailPartDoubles = 2 * 16 * 5 * 32;
+__device__ __forceinline__ double* tail_part_smem(int parity) {
+  return tail_rows()->part + parity * (16 * 5 * 32);
 }
 static __device__ __noinline__ Ctrl* tail_ctrl() {
   __shared__ Ctrl c;
@@ -1886,20 +1890,14 @@ static __device__ __noinline__ Ctrl* tail_ctrl_in() {
   return &c;
 }
 
-// Copies CTA 0's decided control block into every CTA's tail_ctrl_in
-// (called by the 32 lanes of warp 0 of CTA 0).
-static __device__ void tail_broadcast_ctrl(int lane) {
+// Publishes the decided control block to this CTA's next pass (called by
+// the 32 lanes of warp 0; every CTA decides for itself).
+static __device__ void tail_commit_ctrl(int lane) {
   constexpr int kWords = (int)(sizeof(Ctrl) / 8);
   const unsigned long long* src = reinterpret_cast<const unsigned long long*>(tail_ctrl());
-  auto cluster = cooperative_groups::this_cluster();
-  const int cl = (int)cluster.num_blocks();
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(tail_ctrl_in());
   __syncwarp();
-  for (int k = lane; k < cl * kWords; k += 32) {
-    const int rank = k / kWords, word = k - rank * kWords;
-    unsigned long long* dst =
-        reinterpret_cast<unsigned long long*>(cluster.map_shared_rank(tail_ctrl_in(), rank));
-    dst[word] = src[word];
-  }
+  for (int k = lane; k < kWords; k += 32) dst[k] = src[k];
 }
 
 // Copies rows [r0, r1) of a CSR into shared memory at *cursor; returns
@@ -1964,12 +1962,13 @@ static __device__ void tail_setup(const Params& P, char* dyn, int dyn_bytes) {
 // Sums of this CTA's rows for NS columns-sums, reduced over the CTA in a
 // fixed tree and stored to P.tail_part[cta][k0 + s][jj].
 template <int W, int NS, int LL, int NT>
-__device__ __forceinline__ void tail_publish(const Params& P, double (&acc)[NS][Geo<W>::V],
-                                             int k0, double* red) {
+__device__ __forceinline__ void tail_publish(const Params& P, const Ctrl& C,
+                                             double (&acc)[NS][Geo<W>::V], int k0, double* red) {
   using Gm = Geo<W, LL, NT>;
   constexpr int NW = NT / 32;
-  // CTA 0's partial array, through distributed shared memory
-  double* dst = cooperative_groups::this_cluster().map_shared_rank(tail_part_smem(), 0);
+  auto cluster = cooperative_groups::this_cluster();
+  const int cl = (int)cluster.num_blocks();
+  double* part = tail_part_smem((int)(C.passes & 1));
   constexpr int V = Gm::V, L = Gm::L;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #pragma unroll
@@ -1986,6 +1985,7 @@ __device__ __forceinline__ void tail_publish(const Params& P, double (&acc)[NS][
       for (int v = 0; v < V; ++v) red[(warp * NS + s) * W + lane * V + v] = acc[s][v];
   }
   __syncthreads();
+  // this CTA's sums for the live slots, then one copy into every CTA
   for (int t = tid; t < NS * W; t += NT) {
     const int s = t / W, jj = t - s * W;
     double sum = 0.0;
@@ -1993,7 +1993,14 @@ __device__ __forceinline__ void tail_publish(const Params& P, double (&acc)[NS][
 #pragma unroll
       for (int wp = 0; wp < NW; ++wp) sum = __dadd_rn(sum, red[(wp * NS + s) * W + jj]);
     }
-    dst[(blockIdx.x * 5 + k0 + s) * 32 + jj] = sum;
+    red[NW * NS * W + t] = sum;
+  }
+  __syncthreads();
+  for (int t = tid; t < cl * NS * W; t += NT) {
+    const int rank = t / (NS * W), u = t - rank * (NS * W);
+    const int s = u / W, jj = u - s * W;
+    double* dst = cluster.map_shared_rank(part, rank);
+    dst[(blockIdx.x * 5 + k0 + s) * 32 + jj] = red[NW * NS * W + u];
   }
   __syncthreads();
 }
@@ -2025,7 +2032,7 @@ static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* re
       for (int i = r0 + g; i < r1; i += G) op.row(0, i, 0, li, acc);
     }
     tail_mark(P, 2);
-    tail_publish<W, 2, LL, NT>(P, acc, 0, red);
+    tail_publish<W, 2, LL, NT>(P, C, acc, 0, red);
     tail_mark(P, 3);
   }
   cluster_sync_all();
@@ -2051,7 +2058,7 @@ static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* re
       for (int i = r0 + g; i < r1; i += G) op.row(0, i, 0, li, acc);
     }
     tail_mark(P, 5);
-    tail_publish<W, 3, LL, NT>(P, acc, 2, red);
+    tail_publish<W, 3, LL, NT>(P, C, acc, 2, red);
     tail_mark(P, 6);
   }
   cluster_sync_all();
@@ -2060,12 +2067,17 @@ static __device__ void tail_rows_pass(const Params& P, const Ctrl& C, double* re
 }
 
 // decide_body's logic for a plain pass (no check) with active <= 32, run
-// by warp 0 of CTA 0: lane j owns slot j.
+// by warp 0 of EVERY CTA on its own copy of the partials (the computation is
+// deterministic, so all CTAs reach the same control block without a
+// broadcast or a cluster barrier): lane j owns slot j. Global side effects
+// (weights, restart log) are CTA 0's; a weight change is applied to every
+// CTA's shared descriptors here, so no CTA re-reads P.w in the loop.
 static __device__ void tail_decide(const Params& P) {
   const int lane = threadIdx.x;
   Ctrl& C = *tail_ctrl();
   unsigned long long tdbg = 0;
-  if (P.dbg && lane == 0) tdbg = gtime();
+  const bool trace = P.dbg && blockIdx.x == 0 && lane == 0;
+  if (trace) tdbg = gtime();
   if (lane == 0) C = *tail_ctrl_in();
   __syncwarp();
   const int active = C.active;
@@ -2074,8 +2086,9 @@ static __device__ void tail_decide(const Params& P) {
   int err = 0;
   if (lane < active) {
     // fold the CTA partials in CTA order (sequential, fixed)
+    const double* part = tail_part_smem((int)(C.passes & 1));
     for (int c = 0; c < cl; ++c) {
-      const double* tp = tail_part_smem() + c * 5 * 32 + lane;
+      const double* tp = part + c * 5 * 32 + lane;
       dx2 = __dadd_rn(dx2, tp[0]);
       xa2 = __dadd_rn(xa2, tp[32]);
       dy2 = __dadd_rn(dy2, tp[64]);
@@ -2093,7 +2106,7 @@ static __device__ void tail_decide(const Params& P) {
     ts[5 * 32 + lane] = r;
   }
   const bool bad = __any_sync(0xffffffffu, err != 0);
-  if (P.dbg && lane == 0) {  // diagnostic split of the fast decide (BATCHLP_TAIL_TRACE)
+  if (trace) {  // diagnostic split of the fast decide (BATCHLP_TAIL_TRACE)
     const unsigned long long now = gtime();
     P.dbg[14] += now - tdbg;
     tdbg = now;
@@ -2110,7 +2123,7 @@ static __device__ void tail_decide(const Params& P) {
       C.error = loop_err ? BL_ERR_LOGIC : BL_ERR_DOMAIN;
       C.done = 1;
     }
-    tail_broadcast_ctrl(lane);
+    tail_commit_ctrl(lane);
     return;
   }
   // averaged residual: sequential sum in slot order (ordered_sum, count <= 256);
@@ -2136,10 +2149,17 @@ static __device__ void tail_decide(const Params& P) {
   }
   if (reason >= 0 && lane < active) {
     const double ar = first ? r : tail_ar()[lane];
-    if (r <= ar) P.w[lane] = smoothed_weight(w, sqrt(xa2), sqrt(ya2), P.theta);
+    if (r <= ar) {
+      const double nw = smoothed_weight(w, sqrt(xa2), sqrt(ya2), P.theta);
+      if (blockIdx.x == 0) P.w[lane] = nw;
+      // StepParams (solver.hpp:58-59), as load_col computes them
+      tail_w()[lane] = nw;
+      tail_cols(0)[lane].step = P.eta / nw;
+      tail_cols(1)[lane].step = P.eta * nw;
+    }
   }
   __syncwarp();  // every lane has read the control block
-  if (P.dbg && lane == 0) P.dbg[15] += gtime() - tdbg;
+  if (trace) P.dbg[15] += gtime() - tdbg;
   if (lane == 0) {
     if (first) C.mean_anchor = mean;
     C.mean = mean;
@@ -2150,7 +2170,7 @@ static __device__ void tail_decide(const Params& P) {
     C.n_finished = 0;
     C.hash_pending = 0;
     if (reason >= 0) {
-      if (C.log_count < P.log_cap) {
+      if (blockIdx.x == 0 && C.log_count < P.log_cap) {
         bl_restart_event& e = P.log[C.log_count];
         e.at_iteration = C.total_k;
         e.reason = reason;
@@ -2163,6 +2183,7 @@ static __device__ void tail_decide(const Params& P) {
       C.inner_k = 0;
       C.restarts += 1;
       C.col_epoch += 1;
+      tail_rows()->epoch = C.col_epoch;  // the descriptors were updated above
     } else {
       C.alpha_used = C.alpha;
       C.cur ^= 1;
@@ -2176,7 +2197,7 @@ static __device__ void tail_decide(const Params& P) {
     C.check = (C.total_k % P.period == 0) || C.at_cap;
     C.cert_pending = 0;
   }
-  tail_broadcast_ctrl(lane);
+  tail_commit_ctrl(lane);
 }
 
 // One fast tail pass on the cluster (all CTAs of NT threads).
@@ -2203,9 +2224,9 @@ static __device__ void tail_pass(const Params& P, const Ctrl& C, double* red) {
   const int Lsel = pass_lanes<W>(C.active);
   tail_mark(P, 1);
   BL_DISPATCH_L(W, Lsel, (tail_rows_pass<W, LL_, NT>(P, C, red)));
-  if (blockIdx.x == 0 && threadIdx.x < 32) tail_decide(P);
+  if (threadIdx.x < 32) tail_decide(P);
   tail_mark(P, 8);
-  cluster_sync_all();
+  __syncthreads();  // this CTA's next pass sees its decided control block
   tail_phase(2);
   tail_mark(P, 9);
 }
@@ -2228,13 +2249,16 @@ __device__ __forceinline__ bool tail_fast_ok(const Params& P, const Ctrl& C, int
 #define BL_TAIL_THREADS 512
 #endif
 constexpr int kTailThreads = BL_TAIL_THREADS;
-constexpr int kTailRedBytes = (kTailThreads / 32) * 3 * 32 * 8;
+// per-warp sums plus one row of CTA sums
+constexpr int kTailRedBytes = (kTailThreads / 32 + 1) * 3 * 32 * 8;
+constexpr int kTailPartBytes = kTailPartDoubles * 8;
 template <int W>
 __global__ void __launch_bounds__(kTailThreads, 1) k_tail_fast(Params P, int tail_smem) {
   // dynamic shared memory: the per-warp reduction scratch, then the CSR cache
   extern __shared__ __align__(16) char tail_dyn[];
   double* red = reinterpret_cast<double*>(tail_dyn);
-  tail_setup(P, tail_dyn + kTailRedBytes, tail_smem);
+  if (threadIdx.x == 0) tail_rows()->part = reinterpret_cast<double*>(tail_dyn + kTailRedBytes);
+  tail_setup(P, tail_dyn + kTailRedBytes + kTailPartBytes, tail_smem);
   if (threadIdx.x == 0) *tail_ctrl_in() = load_ctrl(P.ctrl);
   __syncthreads();
   // Profiling: fold the stamps a generic pass left (CTA 0), then time the
@@ -2249,9 +2273,11 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail_fast(Params P, int tai
     const Ctrl C0 = *tail_ctrl_in();
     prof_fold(P, C0, threadIdx.x, gtime());
   }
-  if (blockIdx.x == 0 && threadIdx.x < W) tail_ar()[threadIdx.x] = P.anchor_resid[threadIdx.x];
+  if (threadIdx.x < W) tail_ar()[threadIdx.x] = P.anchor_resid[threadIdx.x];
   if (threadIdx.x == 0) tr->npass = 0;
-  __syncthreads();
+  // every CTA of the cluster has started before any pushes into its shared
+  // memory (distributed shared memory rule)
+  cluster_sync_all();
   for (;;) {
     tail_mark(P, 0);
     const Ctrl C = *tail_ctrl_in();
@@ -2597,13 +2623,13 @@ cudaError_t WLaunch<W>::tail_fast(const Params& P, cudaStream_t s, int tail_smem
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           tail_smem + kTailRedBytes);
+  const int dyn = tail_smem + kTailRedBytes + kTailPartBytes;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P.grid);
   cfg.blockDim = dim3(kTailThreads);
-  cfg.dynamicSmemBytes = tail_smem + kTailRedBytes;
+  cfg.dynamicSmemBytes = dyn;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
