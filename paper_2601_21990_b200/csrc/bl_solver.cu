@@ -128,6 +128,10 @@ struct bl_ctx {
   cudaGraph_t tail_graph = nullptr;
   bl::Params tail_params{};
   int tail_smem = -1;
+  // power-iteration graph cache (16 steps), keyed by its parameters
+  cudaGraphExec_t pi_exec = nullptr;
+  bl::Params pi_params{};
+  const void* pi_ptrs[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace {
@@ -253,9 +257,27 @@ double device_spectral_norm(bl_ctx* ctx, bl_problem* p) {
   ck(cudaMemsetAsync(P.counters, 0, sizeof(int) * 64, s), "memset counters");
   P.colsum = static_cast<double*>(ctx->buf[bl_ctx::B_TMP1].ensure(sizeof(double) * 2));
   P.Kp = 2;
+  // 16 steps (7 kernels each) per host check, replayed from a CUDA graph:
+  // one launch instead of 112; rebuilt only when the buffers or the problem
+  // change (bl_problem_assign keeps them)
+  const void* ptrs[4] = {V, U, Wv, st};
+  if (!ctx->pi_exec || std::memcmp(&ctx->pi_params, &P, sizeof(P)) != 0 ||
+      std::memcmp(ctx->pi_ptrs, ptrs, sizeof(ptrs)) != 0) {
+    if (ctx->pi_exec) cudaGraphExecDestroy(ctx->pi_exec);
+    ctx->pi_exec = nullptr;
+    cudaGraph_t g;
+    ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "pi capture");
+    for (int k = 0; k < 16; ++k) bl::launch_pi_step(P, s, V, U, Wv, st);
+    ck(cudaStreamEndCapture(s, &g), "pi capture end");
+    const cudaError_t e = cudaGraphInstantiate(&ctx->pi_exec, g, 0);
+    cudaGraphDestroy(g);
+    ck(e, "pi graph instantiate");
+    ctx->pi_params = P;
+    std::memcpy(ctx->pi_ptrs, ptrs, sizeof(ptrs));
+  }
   bl::PiState hst[2];
   for (int it = 0; it < 5000; it += 16) {
-    for (int k = 0; k < 16; ++k) bl::launch_pi_step(P, s, V, U, Wv, st);
+    ck(cudaGraphLaunch(ctx->pi_exec, s), "pi graph launch");
     ck(cudaMemcpyAsync(hst, st, sizeof(hst), cudaMemcpyDeviceToHost, s), "pi read");
     ck(cudaStreamSynchronize(s), "pi sync");
     if (hst[0].done && hst[1].done) break;
@@ -1099,6 +1121,7 @@ void bl_ctx_destroy(bl_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   free_graph(ctx);
   free_tail_graph(ctx);
+  if (ctx->pi_exec) cudaGraphExecDestroy(ctx->pi_exec);
   for (auto& b : ctx->buf) b.release();
   if (ctx->h_ctrl) cudaFreeHost(ctx->h_ctrl);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
