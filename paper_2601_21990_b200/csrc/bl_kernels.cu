@@ -164,6 +164,11 @@ __global__ void k_pi_tick(PiState* st) {
   }
 
 int max_ctas_per_sm() { return WLaunch<32>::row_ctas_per_sm(); }
+int plain_ctas_per_sm(int W) {
+  int r = 1;
+  BL_DISPATCH_W(W, r = WLaunch<W_>::plain_ctas_per_sm());
+  return r;
+}
 
 static int fill_grid(long long work) {
   long long g = (work + 255) / 256;

@@ -1397,8 +1397,10 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
       C.at_cap = C.total_k >= P.max_it;
       C.check = (C.total_k % P.period == 0) || C.at_cap;
       const int nba = (C.active + P.W - 1) / P.W;
-      C.Rp = items_per_block(P.n, P.m, P.W, P.grid, nba, P.l2_budget);
-      C.Rd = items_per_block(P.m, P.n, P.W, P.grid, nba, P.l2_budget);
+      C.Rp = rounds_adjust(items_per_block(P.n, P.m, P.W, P.grid, nba, P.l2_budget), nba,
+                           P.grid_run);
+      C.Rd = rounds_adjust(items_per_block(P.m, P.n, P.W, P.grid, nba, P.l2_budget), nba,
+                           P.grid_run);
       C.Rc = C.Rp;
     }
     C.cert_pending = 0;
@@ -2441,6 +2443,7 @@ struct WLaunch {
   static cudaError_t loop_cluster(const Params& P, cudaStream_t s, int tail_smem);
   static int max_tail_cluster();
   static int row_ctas_per_sm();
+  static int plain_ctas_per_sm();
   static cudaError_t tail_fast(const Params& P, cudaStream_t s, int tail_smem);
 };
 
@@ -2639,6 +2642,17 @@ cudaError_t WLaunch<W>::tail_fast(const Params& P, cudaStream_t s, int tail_smem
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, fn, P, tail_smem);
+}
+
+// Resident CTAs per SM of the plain-pass row kernels (their launch grid, grid_of).
+template <int W>
+int WLaunch<W>::plain_ctas_per_sm() {
+  int a = 1, b = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_primal<W, false>, kBlock, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_dual<W, false>, kBlock, 0);
+  int occ = a < b ? a : b;
+  if (occ > 4) occ = 4;
+  return occ < 1 ? 1 : occ;
 }
 
 // Resident CTAs per SM of the widest row kernels (grid of the plain kernels).

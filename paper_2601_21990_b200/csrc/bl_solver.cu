@@ -836,6 +836,9 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.trace = cfg.trace_iterates != 0;
   P.vectors = vec;
   P.grid = use_graph ? grid : grid_loop;
+  // the graph / step drivers' plain row kernels launch at their own occupancy
+  P.grid_run = use_graph ? ctx->sms * bl::plain_ctas_per_sm(W) : 0;
+  if (std::getenv("BATCHLP_NO_ROUNDS")) P.grid_run = 0;
   P.l2_budget = l2_budget;
   P.handover_bytes = (mode_loop == 0) ? kHandoverBytes : 0.0;
   // TMA-gather kernels for W = 32 (bl_tma.cuh), opt-in with BATCHLP_TMA=1:
@@ -937,8 +940,10 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   c0.anchor_reset = 1;
   {
     const int nba = (active + W - 1) / W;
-    c0.Rp = bl::items_per_block(n, m, W, P.grid, nba, l2_budget);
-    c0.Rd = bl::items_per_block(m, n, W, P.grid, nba, l2_budget);
+    c0.Rp = bl::rounds_adjust(bl::items_per_block(n, m, W, P.grid, nba, l2_budget), nba,
+                              P.grid_run);
+    c0.Rd = bl::rounds_adjust(bl::items_per_block(m, n, W, P.grid, nba, l2_budget), nba,
+                              P.grid_run);
     c0.Rc = c0.Rp;
   }
   *ctx->h_ctrl = c0;
@@ -954,6 +959,7 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
         // no-op launch when the graph already finished the batch)
         bl::Params Q = P;
         Q.grid = grid_loop;
+        Q.grid_run = 0;
         Q.handover_bytes = 0.0;
         Q.use_graph = 0;
         Q.tail_blocks = use_cluster ? tail_blocks : 0;
@@ -964,6 +970,7 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
         // batch is already finished)
         bl::Params Q = P;
         Q.grid = tail_cluster;
+        Q.grid_run = 0;
         Q.handover_bytes = 0.0;
         Q.use_graph = 0;
         Q.tail_blocks = 0;
