@@ -2343,6 +2343,13 @@ __global__ void __launch_bounds__(kBlock) k_loop(Params P, int tail_smem) {
     // been written by a driver with another grid)
     C.Rp = items_per_block(P.n, P.m, W, grid, nba, P.l2_budget);
     C.Rd = items_per_block(P.m, P.n, W, grid, nba, P.l2_budget);
+#ifndef BL_LOOP_ROUNDS
+#define BL_LOOP_ROUNDS 1
+#endif
+    if (!CL && BL_LOOP_ROUNDS) {  // the grid-stride walk runs in rounds of this grid
+      C.Rp = rounds_adjust(C.Rp, nba, grid);
+      C.Rd = rounds_adjust(C.Rd, nba, grid);
+    }
     C.Rc = C.Rp;
     const int Lsel = CL ? pass_lanes<W>(C.active) : Geo<W>::L;
     BL_DISPATCH_L(W, Lsel, (loop_rows<W, LL_>(P, C, red, sync)));
