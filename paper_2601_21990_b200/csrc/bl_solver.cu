@@ -741,7 +741,8 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   //   latency-bound rest, then (<= tail_blocks active column blocks) one
   //   thread-block cluster for the last few LPs; 1 graph only;
   //   2 host-stepped; 3 persistent grid + cluster; 4 cluster only.
-  constexpr double kHandoverBytes = 16.0 * (1 << 20);
+  double kHandoverBytes = 16.0 * (1 << 20);
+  if (const char* e = std::getenv("BATCHLP_HANDOVER_MB")) kHandoverBytes = std::atof(e) * (1 << 20);
   int mode_loop = 0;
   if (const char* e = std::getenv("BATCHLP_LOOP")) {
     if (std::strcmp(e, "graph") == 0) mode_loop = 1;
