@@ -5,11 +5,12 @@
                   [--impl ours|reference]
 
 One step = one batched solve of the whole workload (all LPs of the config to
-their termination status). Default workload: BASELINE.json configs[1], OBBT
-with 2n = 4000 LPs on a synthetic m = n = 2000 LP (fits one GPU). Under
-torchrun (N > 1) the columns are sharded across ranks (no collective in the
-iteration loop, one all_gather of per-LP scalars at the end); value = all LPs
-/ max-over-ranks step time.
+their termination status). Default workload: BASELINE.json configs[3], the
+north-star config C4: strong branching K = 1024 on a synthetic m = 100k,
+n = 200k sparse cover LP (the largest configuration; ~20 GB of HBM on one
+GPU). Under torchrun (N > 1) the K columns are sharded across ranks (strong
+scaling: no collective in the iteration loop, one all_gather of per-LP
+scalars at the end); value = all LPs / max-over-ranks step time.
 
   value     device-resident solve: problem already in HBM, time from CUDA
             events recorded on the solver's own stream (max over ranks)
@@ -19,6 +20,17 @@ iteration loop, one all_gather of per-LP scalars at the end); value = all LPs
   roofline  dominant kernel (in-situ %globaltimer spans inside the graph)
             algorithmic bytes / time vs MEASURED_PEAKS.json hbm_gbs
   cpu_baseline  the reference CPU path (oracle/_ref) on a bounded sample
+
+CPU reference timing (cpu_baseline and --impl reference):
+  c1, c2     the reference solve_batch to full convergence (the --impl
+             reference arm solves the WHOLE batch; cpu_baseline a sample)
+  c3, c4, c5 time-boxed: 2x16 columns of the batch for 64 batch iterations at
+             eps 1e-30 give t = seconds per column-iteration; LPs/s is
+             EXTRAPOLATED as K / (t x sum of per-LP iterations of the GPU run)
+             (the GPU's per-LP iteration counts, which match the reference's
+             within 10 %, are recorded in profiles/gpu_iterations.json)
+The reference arm never loads the CUDA library: its instances come from the
+host-only build of the same generators (oracle/_ref/libbl_inputs.so).
 """
 from __future__ import annotations
 
@@ -44,9 +56,12 @@ UNIT = "LPs/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--K", type=int, default=0, help="batch width override (C5 sweep)")
+    ap.add_argument("--record-iterations", action="store_true",
+                    help="write this run's per-LP iterations to profiles/gpu_iterations.json")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=0,
                     help="variables (OBBT) / branch pairs (FSB) in the CPU sample")
@@ -73,8 +88,40 @@ def peaks():
 # ---------------------------------------------------------------------------
 # workloads
 # ---------------------------------------------------------------------------
-def build_workload(name: str, bl, I):
-    """(BatchProblem, presets, description dict) of a config."""
+EXTRAPOLATED = ("c3", "c4", "c5")  # CPU time-boxed; c1/c2 converge
+ITERATIONS_FILE = os.path.join(ROOT, "profiles", "gpu_iterations.json")
+
+
+def subset_batch(bl, batch, presets, cols):
+    """The LPs `cols` of a batch as a standalone batch (same LPs, new column
+    order): signed-unit objectives become objective-entry overrides on a
+    zero base objective. Returns (LpProblem, BatchProblem, presets)."""
+    import dataclasses
+    from paper_2601_21990_b200.problem import (BatchProblem, ColumnOverride, LpProblem,
+                                                ObjectiveMode, OverrideKind)
+    colset = {c: i for i, c in enumerate(cols)}
+    base = batch.base()
+    ovs = []
+    if batch.objective_mode() == ObjectiveMode.kSignedUnitColumns:
+        n = base.num_cols()
+        lp = LpProblem(base.A, np.zeros(n), base.row_bounds, base.var_bounds)
+        for i, c in enumerate(cols):
+            var, sign = (c, 1.0) if c < n else (c - n, -1.0)
+            ovs.append(ColumnOverride(i, OverrideKind.kObjectiveEntry, var, sign))
+    else:
+        lp = base
+        for o in batch.overrides():
+            if o.column in colset:
+                ovs.append(ColumnOverride(colset[o.column], o.kind, o.variable, o.value))
+        ovs.sort(key=lambda o: o.column)
+    pre = [dataclasses.replace(q, column=colset[q.column]) for q in presets
+           if q.column in colset]
+    return lp, BatchProblem(lp, len(cols), ObjectiveMode.kSharedObjective, ovs), pre
+
+
+def build_workload(name: str, bl, I, K: int = 0, root_x=None):
+    """(LpProblem, BatchProblem, presets, SolverConfig, spec) of a config.
+    K overrides the batch width of an FSB config (the C5 sweep)."""
     spec = I.CONFIGS[name]
     p = I.config_problem(name)
     if spec.kind == "obbt":
@@ -83,15 +130,45 @@ def build_workload(name: str, bl, I):
         return p, ob.batch, ob.presets, cfg, spec
     # FSB: branch on the first K/2 fractional variables of the root relaxation
     # (C1: the reference recipe of SURVEY §8(d); large configs: x = 0.5 on
-    # the first K/2 columns, acceptance.cpp:209-212).
-    K = spec.K
+    # the first K/2 columns, acceptance.cpp:209-212). An odd K (sweep) keeps
+    # the first K columns of the ceil(K/2)-pair batch.
+    K = K or spec.K
+    pairs = (K + 1) // 2
     if name == "c1":
-        root = bl.solve(p)
-        x, frac = I.synthetic_branch_point(p, K // 2, root.x)
+        if root_x is None:
+            root_x = bl.solve(p).x
+        x, frac = I.synthetic_branch_point(p, pairs, root_x)
     else:
-        x, frac = I.synthetic_branch_point(p, K // 2)
+        x, frac = I.synthetic_branch_point(p, pairs)
     fb = bl.build_fsb_batch(bl.FsbRequest(p, x, frac))
-    return p, fb.batch, fb.presets, bl.SolverConfig(), spec
+    batch, presets = fb.batch, fb.presets
+    if batch.batch_width() != K:
+        _, batch, presets = subset_batch(bl, batch, presets, list(range(K)))
+    return p, batch, presets, bl.SolverConfig(), spec
+
+
+def config_block(name, spec, p, batch, cfg, world):
+    """The `config` object of the JSON line; identical in both arms."""
+    return {"workload": f"{name}: {spec.description}", "K": batch.batch_width(),
+            "m": p.num_rows(), "n": p.num_cols(), "nnz": p.A.nnz(),
+            "eps_opt": cfg.eps_opt, "eps_dual": cfg.effective_eps_dual(),
+            "l2": "flushed between GPU steps (256 MiB write)",
+            "parallelism": f"LP columns sharded x{world} (strong scaling), A replicated"}
+
+
+def sample_columns(spec, batch, pairs):
+    """Columns of the bounded CPU sample: the first `pairs` variables in both
+    directions (OBBT min/max, FSB up/down branches)."""
+    width = batch.batch_width()
+    if spec.kind == "obbt":
+        n = batch.base().num_cols()
+        nv = min(pairs, n)
+        return list(range(nv)) + list(range(n, n + nv))
+    half = width // 2
+    pairs = min(pairs, half)
+    if pairs == 0:
+        return list(range(width))
+    return list(range(pairs)) + list(range(half, half + pairs))
 
 
 class ClockSampler:
@@ -148,48 +225,101 @@ def flush_l2(torch, dev):
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference (oracle/_ref) on a bounded sample
 # ---------------------------------------------------------------------------
-def cpu_sample(name, p, batch, presets, cfg, spec, sample):
-    """Runs the compiled reference on a column sample of the workload;
-    returns (LPs/s, description, threads)."""
+def _ref_presets(presets):
+    return [(q.column, int(q.result.status), q.result.objective) for q in presets]
+
+
+def cpu_converged(bl, ref, batch, presets, cfg, cols=None):
+    """The reference solve_batch (oracle/_ref) to full convergence on the
+    whole batch or on the LPs `cols`; returns (LPs/s, seconds, summary)."""
+    if cols is not None:
+        _, batch, presets = subset_batch(bl, batch, presets, cols)
+    lp = batch.base()
+    t0 = time.perf_counter()
+    r = ref.solve_batch(lp, batch.batch_width(), int(batch.objective_mode()),
+                        batch.overrides(), cfg, _ref_presets(presets), vectors=False)
+    el = time.perf_counter() - t0
+    return batch.batch_width() / el, el, r
+
+
+def cpu_timebox(bl, ref, batch, presets, cfg, cols, iterations=64):
+    """SURVEY §8(d) time box: the reference solve_batch on the LPs `cols`
+    for `iterations` batch iterations with the tolerances at 1e-30 (nothing
+    terminates); returns (seconds per column-iteration, seconds, summary)."""
+    import dataclasses
+    _, sb, sp = subset_batch(bl, batch, presets, cols)
+    c = dataclasses.replace(cfg, eps_opt=1e-30, eps_dual=1e-30, eps_infeas=1e-30,
+                            max_iterations=iterations)
+    t0 = time.perf_counter()
+    r = ref.solve_batch(sb.base(), sb.batch_width(), 0, sb.overrides(), c, _ref_presets(sp),
+                        vectors=False)
+    el = time.perf_counter() - t0
+    active = sb.batch_width() - len(sp)
+    return el / max(active * r.iterations, 1), el, r
+
+
+def cpu_threads():
     threads = os.cpu_count() or 1
     os.environ["BATCHLP_THREADS"] = str(threads)
-    from oracle import ref
-    from paper_2601_21990_b200 import distributed as D
+    return threads
+
+
+def cpu_baseline(name, bl, ref, batch, presets, cfg, spec, sum_iterations, pairs=0,
+                 full=False):
+    """One CPU measurement of the reference path on this workload:
+    (LPs/s, seconds, description). c1/c2: full convergence, of the whole
+    batch when `full`, else of a bounded sample; c3-c5: time box and
+    extrapolation over `sum_iterations` (the GPU run's per-LP total)."""
+    threads = cpu_threads()
     width = batch.batch_width()
-    if spec.kind == "obbt":
-        nv = sample or 600
-        n = p.num_cols()
-        cols = list(range(nv)) + list(range(n, n + nv))
-    else:
-        pairs = sample or min(width // 2, 16)
-        half = width // 2
-        cols = list(range(pairs)) + list(range(half, half + pairs))
-    # rewrite the sample as a shared-objective batch (same LPs)
-    from paper_2601_21990_b200.problem import ColumnOverride, LpProblem, OverrideKind
-    colset = {c: i for i, c in enumerate(cols)}
-    base = batch.base()
-    ovs = []
-    if batch.objective_mode() == 1:  # signed unit: zero base objective + entries
-        n = base.num_cols()
-        lp = LpProblem(base.A, np.zeros(n), base.row_bounds, base.var_bounds)
-        for i, c in enumerate(cols):
-            var, sign = (c, 1.0) if c < n else (c - n, -1.0)
-            ovs.append(ColumnOverride(i, OverrideKind.kObjectiveEntry, var, sign))
-    else:
-        for o in batch.overrides():
-            if o.column in colset:
-                ovs.append(ColumnOverride(colset[o.column], o.kind, o.variable, o.value))
-        lp = base
-    pre = [(colset[q.column], int(q.result.status), q.result.objective) for q in presets
-           if q.column in colset]
-    t0 = time.perf_counter()
-    r = ref.solve_batch(lp, len(cols), 0, ovs, cfg, pre, vectors=False)
-    el = time.perf_counter() - t0
-    desc = (f"reference solve_batch (oracle/_ref, g++ -O3) on {len(cols)} of {width} LPs "
-            f"({'variables 0..' + str(nv - 1) + ' both directions' if spec.kind == 'obbt' else str(len(cols) // 2) + ' branch pairs'}), "
+    if name in EXTRAPOLATED:
+        cols = sample_columns(spec, batch, pairs or 16)
+        t_ci, el, r = cpu_timebox(bl, ref, batch, presets, cfg, cols)
+        value = width / (t_ci * sum_iterations)
+        desc = (f"EXTRAPOLATED: reference solve_batch (oracle/_ref, g++ -O3) time-boxed on "
+                f"{len(cols)} of {width} LPs ({len(cols) // 2} branch pairs) for "
+                f"{r.iterations} batch iterations at eps 1e-30: {el:.2f} s = "
+                f"{t_ci * 1e3:.3f} ms per column-iteration; LPs/s = K / (t x "
+                f"{sum_iterations} per-LP iterations of the GPU run); "
+                f"BATCHLP_THREADS={threads}")
+        return value, el, desc, threads
+    if full:
+        value, el, r = cpu_converged(bl, ref, batch, presets, cfg)
+        desc = (f"reference solve_batch (oracle/_ref, g++ -O3) on all {width} LPs, full "
+                f"convergence, {r.iterations} batch iterations, {el:.2f} s, "
+                f"BATCHLP_THREADS={threads}")
+        return value, el, desc, threads
+    cols = sample_columns(spec, batch, pairs or (600 if spec.kind == "obbt" else 16))
+    value, el, r = cpu_converged(bl, ref, batch, presets, cfg, cols)
+    desc = (f"reference solve_batch (oracle/_ref, g++ -O3) on a sample of {len(cols)} of "
+            f"{width} LPs (the first {len(cols) // 2} "
+            f"{'variables, both directions' if spec.kind == 'obbt' else 'branch pairs'}), "
             f"full convergence, {r.iterations} batch iterations, {el:.2f} s, "
             f"BATCHLP_THREADS={threads}")
-    return len(cols) / el, desc, threads, el
+    return value, el, desc, threads
+
+
+def recorded_iterations(name, K):
+    """Sum of per-LP iterations of a recorded GPU run of this workload."""
+    try:
+        with open(ITERATIONS_FILE) as f:
+            d = json.load(f).get(f"{name}:K={K}")
+        return int(d["sum_iterations"]) if d else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def record_iterations(name, K, summary, extra):
+    try:
+        with open(ITERATIONS_FILE) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        d = {}
+    its = [int(r.iterations) for r in summary.per_problem]
+    d[f"{name}:K={K}"] = {"sum_iterations": int(sum(its)), "batch_iterations":
+                          int(summary.iterations), "per_lp_iterations": its, **extra}
+    with open(ITERATIONS_FILE, "w") as f:
+        json.dump(d, f, indent=1)
 
 
 # ---------------------------------------------------------------------------
@@ -211,7 +341,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    p, batch, presets, cfg, spec = build_workload(args.config, bl, I)
+    p, batch, presets, cfg, spec = build_workload(args.config, bl, I, args.K)
     width = batch.batch_width()
     shard = D.shard_batch(batch, presets, rank, world) if world > 1 else None
     my_batch = shard.batch if shard else batch
@@ -389,31 +519,36 @@ def main():
 
     # ---- CPU baseline (rank 0, N = 1) --------------------------------------
     cpu = None
+    sum_its = sum(int(r.iterations) for r in summaries[-1].per_problem)
+    if rank == 0 and world == 1 and args.record_iterations:
+        record_iterations(args.config, width, summaries[-1],
+                          {"source": "bench.py --record-iterations on one B200",
+                           "loop_passes": int(summaries[-1].loop_passes)})
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, desc, threads, _ = cpu_sample(args.config, p, batch, presets, cfg, spec,
-                                             args.cpu_sample)
-            cpu = {"value": round(v, 3), "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": desc}
+            from oracle import ref
+            v, _, desc, threads = cpu_baseline(args.config, bl, ref, batch, presets, cfg, spec,
+                                               sum_its, args.cpu_sample)
+            cpu = {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "reference",
+                   "extrapolated": args.config in EXTRAPOLATED, "sample": desc}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
     if rank == 0:
-        nnz = p.A.nnz()
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": round(ms_step, 3), "higher_is_better": True,
-            "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, DESIGN.md §5)",
-            "config": {"workload": f"{args.config}: {spec.description}", "K": width,
-                       "m": p.num_rows(), "n": p.num_cols(), "nnz": nnz,
-                       "eps_opt": cfg.eps_opt, "eps_dual": cfg.effective_eps_dual(),
-                       "batch_iterations": summaries[-1].iterations,
-                       "loop_passes": summaries[-1].loop_passes,
-                       "l2": "flushed between steps (256 MiB write)",
-                       "parallelism": f"columns sharded x{world}, A replicated"},
+            "config": config_block(args.config, spec, p, batch, cfg, world),
+            "run": {"batch_iterations": summaries[-1].iterations,
+                    "loop_passes": summaries[-1].loop_passes,
+                    "sum_lp_iterations_rank0": sum_its,
+                    "statuses_rank0": {str(k): v for k, v in sorted(
+                        __import__("collections").Counter(
+                            int(r.status) for r in summaries[-1].per_problem).items())}},
             "e2e": {"value": round(e2e, 3), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d + per_solve_h2d),
                     "d2h_bytes_per_step": int(per_solve_d2h)},
@@ -430,58 +565,61 @@ def main():
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference CPU path (oracle/_ref) on a bounded
-    sample of the same workload, rank 0 only."""
+    """--impl reference: the reference CPU path (oracle/_ref, the reference
+    headers compiled by oracle/Makefile) on the same workload, rank 0 only.
+    Loads nothing from the CUDA package: the instances come from the
+    host-only generator build oracle/_ref/libbl_inputs.so."""
     if rank != 0:
         return
     import paper_2601_21990_b200 as bl
     from paper_2601_21990_b200 import instances as I
     from oracle import ref
-    if not ref.available():
+    gen = os.path.join(ROOT, "oracle", "_ref", "libbl_inputs.so")
+    if not ref.available() or not os.path.exists(gen):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    p, batch, presets, cfg, spec = build_workload_cpu(args.config, bl, I, ref)
-    times, vals, desc, threads = [], [], "", 1
+    I.use_generator_library(gen)
+    root_x = None
+    if args.config == "c1":  # root relaxation from the reference solve
+        root_x = ref.solve(I.config_problem("c1")).per_problem[0].x
+    p, batch, presets, cfg, spec = build_workload(args.config, bl, I, args.K, root_x)
+    width = batch.batch_width()
+    sum_its = None
+    if args.config in EXTRAPOLATED:
+        sum_its = recorded_iterations(args.config, width)
+        if sum_its is None:
+            print(json.dumps({"impl": "reference", "unavailable":
+                              f"no recorded GPU per-LP iterations for {args.config} K={width} "
+                              f"({os.path.relpath(ITERATIONS_FILE, ROOT)})"}))
+            return
     # untimed warm-up steps on a small sample of the same workload (library
-    # load, thread pool, page-in); the timed steps are full bounded samples
+    # load, thread pool, page-in); the timed steps are the full measurement
     warm = max(args.warmup, 3)
+    cols = sample_columns(spec, batch, 2 if spec.kind == "fsb" else 8)
     for _ in range(warm):
-        cpu_sample(args.config, p, batch, presets, cfg, spec, 8 if spec.kind == "obbt" else 1)
+        if args.config in EXTRAPOLATED:
+            cpu_timebox(bl, ref, batch, presets, cfg, cols, iterations=8)
+        else:
+            cpu_converged(bl, ref, batch, presets, cfg, cols)
+    times, vals, desc, threads = [], [], "", 1
     for _ in range(max(args.steps, 1)):
-        v, desc, threads, el = cpu_sample(args.config, p, batch, presets, cfg, spec,
-                                          args.cpu_sample)
+        v, el, desc, threads = cpu_baseline(args.config, bl, ref, batch, presets, cfg, spec,
+                                            sum_its, args.cpu_sample, full=True)
         vals.append(v)
         times.append(el)
     value = len(vals) / sum(1.0 / v for v in vals)
-    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": warm,
             "ms_per_step": round(1e3 * sum(times) / len(times), 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, DESIGN.md §5)",
-            "config": {"workload": f"{args.config}: {spec.description}",
-                       "K": batch.batch_width(), "m": p.num_rows(), "n": p.num_cols()},
-            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads,
+            "config": config_block(args.config, spec, p, batch, cfg, world),
+            "extrapolated": args.config in EXTRAPOLATED,
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads,
                              "kind": "reference", "sample": desc},
-            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
-
-def build_workload_cpu(name, bl, I, ref):
-    """Workload construction without a GPU (for the reference arm): the C1
-    root relaxation comes from the reference solve."""
-    spec = I.CONFIGS[name]
-    p = I.config_problem(name)
-    if spec.kind == "obbt":
-        ob = bl.build_obbt_batch(p, bl.ObbtConfig())
-        return p, ob.batch, ob.presets, bl.ObbtConfig().solver_config(), spec
-    if name == "c1":
-        x0 = ref.solve(p).per_problem[0].x
-        x, frac = I.synthetic_branch_point(p, spec.K // 2, x0)
-    else:
-        x, frac = I.synthetic_branch_point(p, spec.K // 2)
-    fb = bl.build_fsb_batch(bl.FsbRequest(p, x, frac))
-    return p, fb.batch, fb.presets, bl.SolverConfig(), spec
 
 
 if __name__ == "__main__":

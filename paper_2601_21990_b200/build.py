@@ -99,7 +99,7 @@ def build_oracles(verbose: bool = False) -> None:
     where /root/reference exists (the GPU box uses the prebuilt .so)."""
     targets = []
     if os.path.exists(os.path.join(ROOT, "oracle", "batchlp_oracle.c")):
-        targets.append("oracle")
+        targets += ["oracle", "inputs"]
     if os.path.isdir("/root/reference/proj/include"):
         targets.append("ref")
     cmd = ["make", "-s", "-C", os.path.join(ROOT, "oracle"), *targets]

@@ -782,6 +782,9 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
       max_items = std::max(max_items, std::max(a, b));
     }
   }
+  // the initial AX = A X (launch_spmm) picks its own item count per block
+  max_items = std::max(max_items, (size_t)nb * std::max(items_for(m, W, grid),
+                                                       items_for(n, W, grid)));
   P.partials = static_cast<double*>(
       ctx->buf[bl_ctx::B_PART].ensure(sizeof(double) * max_items * 10 * W));
   P.counters = static_cast<int*>(ctx->buf[bl_ctx::B_CNT].ensure(sizeof(int) * (size_t)std::max(nb, 64)));

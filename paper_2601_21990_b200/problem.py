@@ -79,18 +79,55 @@ class Bounds:
         return Bounds.from_arrays(self.lower, self.upper)
 
 
+_INT32_MAX = 2**31 - 1
+
+
+def _index_array(a, what: str) -> np.ndarray:
+    """int32 copy of an index array; values beyond int32 raise (the device
+    CSR is int32, nnz <= INT32_MAX)."""
+    a = np.asarray(a)
+    if a.dtype.kind not in "iu":
+        if a.size and not np.all(np.floor(a) == a):
+            raise InvalidArgument(f"sparse: non-integer {what}")
+    if a.size and (int(a.max()) > _INT32_MAX or int(a.min()) < -_INT32_MAX - 1):
+        raise InvalidArgument(f"sparse: {what} exceed int32 (nnz above INT32_MAX)")
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _check_csr(ptr: np.ndarray, idx: np.ndarray, val: np.ndarray, rows: int, cols: int):
+    """Invariants of detail/csr.hpp from_csr: rows + 1 monotone offsets from
+    0 to nnz, one value per index (InvalidArgument); column indices inside
+    [0, cols) (OutOfRange)."""
+    if (ptr.shape[0] != rows + 1 or idx.shape[0] != val.shape[0] or int(ptr[0]) != 0
+            or int(ptr[-1]) != idx.shape[0] or (rows > 0 and bool(np.any(np.diff(ptr) < 0)))):
+        raise InvalidArgument("sparse: malformed CSR arrays")
+    if idx.size and (int(idx.min()) < 0 or int(idx.max()) >= cols):
+        raise OutOfRange("sparse: column index out of range")
+
+
 class SparseMatrix:
     """CSR matrix with an explicit transpose (sparse.hpp:93-171). Immutable."""
 
     def __init__(self, n_rows, n_cols, offsets, cols, values, t_offsets, t_cols, t_values):
         self._n_rows = int(n_rows)
         self._n_cols = int(n_cols)
-        self.row_offsets = np.ascontiguousarray(offsets, dtype=np.int32)
-        self.col_indices = np.ascontiguousarray(cols, dtype=np.int32)
+        if self._n_rows < 0 or self._n_cols < 0:
+            raise InvalidArgument("sparse: negative dimension")
+        # the arrays are uploaded to the device as they are: check the CSR
+        # invariants first (detail/csr.hpp from_csr), so malformed input
+        # raises instead of reading out of bounds on the GPU
+        self.row_offsets = _index_array(offsets, "offsets")
+        self.col_indices = _index_array(cols, "column indices")
         self.values = np.ascontiguousarray(values, dtype=np.float64)
-        self.t_row_offsets = np.ascontiguousarray(t_offsets, dtype=np.int32)
-        self.t_col_indices = np.ascontiguousarray(t_cols, dtype=np.int32)
+        self.t_row_offsets = _index_array(t_offsets, "transpose offsets")
+        self.t_col_indices = _index_array(t_cols, "transpose column indices")
         self.t_values = np.ascontiguousarray(t_values, dtype=np.float64)
+        _check_csr(self.row_offsets, self.col_indices, self.values, self._n_rows,
+                   self._n_cols)
+        _check_csr(self.t_row_offsets, self.t_col_indices, self.t_values, self._n_cols,
+                   self._n_rows)
+        if self.t_values.shape[0] != self.values.shape[0]:
+            raise InvalidArgument("sparse: malformed CSR arrays")
         for a in (self.row_offsets, self.col_indices, self.values, self.t_row_offsets,
                   self.t_col_indices, self.t_values):
             a.flags.writeable = False
@@ -383,5 +420,5 @@ class ColumnView:
 
 def resolve_column(b: BatchProblem, column: int) -> ColumnView:
     if column < 0 or column >= b.batch_width():
-        raise IndexError("resolve_column: column out of range")
+        raise OutOfRange("resolve_column: column out of range")
     return ColumnView(b.base(), b.objective_mode(), column, b.overrides_for(column))

@@ -279,10 +279,26 @@ class BatchWorkspace:
         self._problems: Dict[int, tuple] = {}
         self._scratch: Optional[DeviceProblem] = None
 
+    @staticmethod
+    def _vectors(p: LpProblem):
+        return (p.objective, p.var_bounds.lower, p.var_bounds.upper, p.row_bounds.lower,
+                p.row_bounds.upper)
+
     def resident(self, p: LpProblem, cache: bool = True) -> DeviceProblem:
+        """The device copy of p. A cached entry is reused only for the same
+        (immutable) matrix AND the same objective and bounds BY VALUE, as
+        the C++ drop-in does (include/batchlp/device.hpp): the reference
+        passes the LpProblem by value, so an edited bound must be seen."""
         key = id(p.A)
         hit = self._problems.get(key)
-        if cache and hit is not None and hit[0] is p.A and hit[2] is p.objective:
+        if cache and hit is not None and hit[0] is p.A:
+            vec = self._vectors(p)
+            if all(a.shape == b.shape and np.array_equal(a, b, equal_nan=True)
+                   for a, b in zip(vec, hit[2])):
+                return hit[1]
+            # same matrix, new vectors: re-upload into the same device problem
+            hit[1].assign(p)
+            self._problems[key] = (p.A, hit[1], tuple(np.array(v, copy=True) for v in vec))
             return hit[1]
         if not cache:
             # a fresh upload every call (the caller's arrays may have changed),
@@ -296,7 +312,8 @@ class BatchWorkspace:
         if cache:
             if len(self._problems) > 8:
                 self._problems.clear()
-            self._problems[key] = (p.A, dp, p.objective)
+            self._problems[key] = (p.A, dp,
+                                   tuple(np.array(v, copy=True) for v in self._vectors(p)))
         return dp
 
 

@@ -94,3 +94,30 @@ def test_benchmark_generators_are_canonical_and_deterministic(ref, gen):
     assert np.array_equal(a.A.t_col_indices, r.A.t_col_indices)
     assert np.array_equal(a.A.t_values, r.A.t_values)
     assert a.A.nnz() >= 800 * 6
+
+
+def test_host_only_generator_build_matches_the_cuda_library():
+    """bench.py's reference arm generates inputs with the host-only build of
+    csrc/bl_generators.cpp (oracle/_ref/libbl_inputs.so) instead of the CUDA
+    library: both builds must produce identical instances."""
+    from paper_2601_21990_b200 import instances as I
+    path = os.path.join(ROOT, "oracle", "_ref", "libbl_inputs.so")
+    assert os.path.exists(path), "oracle/Makefile inputs target not built"
+    cases = [("set_cover", (120, 200, 0.05, 3)), ("sparse_cover", (500, 900, 10, 7)),
+             ("boxed_feasible", (300, 300, 10, 11))]
+    for fn, args in cases:
+        I.use_generator_library(None)
+        a = getattr(I, fn)(*args)
+        I.use_generator_library(path)
+        try:
+            b = getattr(I, fn)(*args)
+        finally:
+            I.use_generator_library(None)
+        for x, y in ((a.A.row_offsets, b.A.row_offsets), (a.A.col_indices, b.A.col_indices),
+                     (a.A.values, b.A.values), (a.A.t_col_indices, b.A.t_col_indices),
+                     (a.A.t_values, b.A.t_values), (a.objective, b.objective),
+                     (a.var_bounds.lower, b.var_bounds.lower),
+                     (a.var_bounds.upper, b.var_bounds.upper),
+                     (a.row_bounds.lower, b.row_bounds.lower),
+                     (a.row_bounds.upper, b.row_bounds.upper)):
+            assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))

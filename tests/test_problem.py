@@ -185,3 +185,36 @@ def test_column_slices_cover_the_batch():
         assert len(s) == world and s[0][0] == 0 and s[-1][1] == width
         assert all(a[1] == b[0] for a, b in zip(s, s[1:]))
         assert max(e - b for b, e in s) - min(e - b for b, e in s) <= 1
+
+
+def test_sparse_matrix_rejects_malformed_csr():
+    """Raw CSR input is validated before it can reach the device
+    (detail/csr.hpp from_csr): malformed arrays -> InvalidArgument, column
+    index out of range -> OutOfRange."""
+    ok = dict(n_rows=2, n_cols=3, offsets=[0, 1, 2], cols=[0, 2], values=[1.0, 2.0],
+              t_offsets=[0, 1, 1, 2], t_cols=[0, 1], t_values=[1.0, 2.0])
+    bl.SparseMatrix(**ok)  # well formed
+    for k, v in (("offsets", [0, 2, 1]), ("offsets", [1, 1, 2]), ("offsets", [0, 1]),
+                 ("values", [1.0]), ("t_offsets", [0, 1, 1, 3]), ("offsets", [0, 1, 3]),
+                 ("cols", [0, 2**33])):
+        bad = dict(ok)
+        bad[k] = v
+        with pytest.raises(bl.InvalidArgument):
+            bl.SparseMatrix(**bad)
+    for k, v in (("cols", [0, 3]), ("cols", [-1, 2]), ("t_cols", [0, 2])):
+        bad = dict(ok)
+        bad[k] = v
+        with pytest.raises(bl.OutOfRange):
+            bl.SparseMatrix(**bad)
+    with pytest.raises(bl.InvalidArgument):
+        bl.SparseMatrix(-1, 3, [0], [], [], [0, 0, 0, 0], [], [])
+
+
+def test_resolve_column_out_of_range_is_out_of_range():
+    A = bl.SparseMatrix.from_triplets([(0, 0, 1.0)], 1, 1)
+    p = bl.LpProblem(A, np.zeros(1), bl.Bounds(1), bl.Bounds(1))
+    b = bl.BatchProblem(p, 2, bl.ObjectiveMode.kSharedObjective)
+    with pytest.raises(bl.OutOfRange):
+        bl.resolve_column(b, 2)
+    with pytest.raises(bl.OutOfRange):
+        bl.resolve_column(b, -1)
