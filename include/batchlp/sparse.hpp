@@ -6,12 +6,14 @@
 //   spmv / spmm      -> bl_spmm       (CSR SpMM kernel, row-major tiles;
 //                                      entries bit-identical to csr_apply,
 //                                      sparse.hpp:176-183)
+//   csr_apply        -> bl_csr_apply  (the same kernel on a bare CsrView)
 //   spectral_norm    -> bl_spectral_norm (device power iteration,
 //                                      sparse.hpp:249-319)
 // BATCHLP_THREADS (sparse.hpp:198-206) has no meaning here and is ignored.
 #ifndef BATCHLP_B200_SPARSE_HPP
 #define BATCHLP_B200_SPARSE_HPP
 
+#include <cstdint>
 #include <span>
 #include <stdexcept>
 
@@ -19,6 +21,17 @@
 #include "batchlp/device.hpp"
 
 namespace batchlp {
+
+// out = M x on a bare view (reference sparse.hpp:173-183): the view need not
+// belong to a resident SparseMatrix, so it is uploaded for this one product.
+inline void csr_apply(const CsrView& mv, const double* x, double* out) {
+  if (mv.n_rows == 0) return;
+  cuda::Context& ctx = cuda::thread_context();
+  cuda::check(ctx.handle(),
+              bl_csr_apply(ctx.handle(), mv.n_rows, mv.n_cols,
+                           static_cast<std::int64_t>(mv.values.size()), mv.offsets.data(),
+                           mv.cols.data(), mv.values.data(), x, out));
+}
 
 // out.col(j) = op(A) x.col(j) for j < active_width; later columns of `out`
 // keep their contents (reference sparse.hpp:213-238).

@@ -203,6 +203,14 @@ int bl_spectral_norm(bl_ctx* ctx, bl_problem* p, double* out);
  * to the reference csr_apply (sparse.hpp:176-183). */
 int bl_spmm(bl_ctx* ctx, const bl_problem* p, int transpose, int32_t width,
             int32_t active, const double* x, double* out);
+/* csr_apply (sparse.hpp:176-183) on a bare CSR view (CsrView, sparse.hpp:28-
+ * 36) that is not an uploaded problem: out = M x for the rows x cols matrix
+ * (rowptr, col, val), computed by the same SpMM kernel (bit-identical to the
+ * reference's stored-order sum). The view is uploaded into grow-only
+ * context scratch on every call. BL_ERR_INVALID_ARGUMENT for malformed
+ * offsets, BL_ERR_OUT_OF_RANGE for a column index outside [0, cols). */
+int bl_csr_apply(bl_ctx* ctx, int32_t rows, int32_t cols, int64_t nnz, const int32_t* rowptr,
+                 const int32_t* col, const double* val, const double* x, double* out);
 /* measure_spmm (tuner.hpp:72-108) on the device: `repetitions` products
  * A X and `repetitions` products A'Y of `width` columns (seeded blocks, two
  * untimed warm-up rounds), timed with CUDA events on the context's stream;

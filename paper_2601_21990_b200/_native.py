@@ -154,6 +154,7 @@ SIGNATURES = {
     ),
     "bl_spectral_norm": (C.c_int, [_P, _P, _DP]),
     "bl_spmm": (C.c_int, [_P, _P, C.c_int, C.c_int32, C.c_int32, _DP, _DP]),
+    "bl_csr_apply": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int64, _IP, _IP, _DP, _DP, _DP]),
     "bl_measure_spmm": (C.c_int, [_P, _P, C.c_int32, C.c_int32, _DP, _DP,
                                   C.POINTER(C.c_int32)]),
     "bl_solve_batch": (

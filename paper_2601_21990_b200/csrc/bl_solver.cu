@@ -132,6 +132,8 @@ struct bl_ctx {
   cudaGraphExec_t pi_exec = nullptr;
   bl::Params pi_params{};
   const void* pi_ptrs[4] = {nullptr, nullptr, nullptr, nullptr};
+  // transient one-orientation CSR of bl_csr_apply
+  bl_problem csr_scratch;
 };
 
 namespace {
@@ -1074,6 +1076,51 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
 // ===========================================================================
 // C-ABI
 // ===========================================================================
+namespace {
+// op(A) x for the first `active` of `width` column-major host columns:
+// tiles them, runs the SpMM kernel, untiles, copies back (bl_spmm,
+// bl_csr_apply).
+void device_spmm(bl_ctx* ctx, const bl_problem* p, bool transpose, int width, int active,
+                 const double* x, double* out) {
+  if (active < 0) active = width;
+  if (active > width) raise(BL_ERR_INVALID_ARGUMENT, "spmm: active width too large");
+  if (active == 0) return;
+  const int rin = transpose ? p->m : p->n, rout = transpose ? p->n : p->m;
+  const int W = pow2_width(width);
+  const int Kp = (width + W - 1) / W * W;
+  cudaStream_t s = ctx->stream;
+  double* tin = static_cast<double*>(ctx->buf[bl_ctx::B_TMP0].ensure(sizeof(double) * ((size_t)rin * Kp + 1)));
+  double* tout = static_cast<double*>(ctx->buf[bl_ctx::B_TMP1].ensure(sizeof(double) * ((size_t)rout * Kp + 1)));
+  double* raw = static_cast<double*>(ctx->buf[bl_ctx::B_WARMX].ensure(
+      sizeof(double) * ((size_t)std::max(rin, rout) * width + 1)));
+  ck(cudaMemcpyAsync(raw, x, sizeof(double) * (size_t)rin * active, cudaMemcpyHostToDevice, s), "x");
+  bl::launch_to_tiled(s, raw, tin, rin, width, W, active);
+  bl::Params P{};
+  P.m = p->m;
+  P.n = p->n;
+  P.rp = p->rp.as<int>();
+  P.ci = p->ci.as<int>();
+  P.cv = p->cv.as<double>();
+  P.trp = p->trp.as<int>();
+  P.tci = p->tci.as<int>();
+  P.tcv = p->tcv.as<double>();
+  P.W = W;
+  P.Kp = Kp;
+  P.grid = ctx->grid;
+  const int nb = Kp / W;
+  const int R = items_for(rout, W, ctx->grid);
+  P.partials = static_cast<double*>(ctx->buf[bl_ctx::B_PART].ensure(sizeof(double) * (size_t)nb * R * 10 * W));
+  P.counters = static_cast<int*>(ctx->buf[bl_ctx::B_CNT].ensure(sizeof(int) * (size_t)std::max(nb, 64)));
+  ck(cudaMemsetAsync(P.counters, 0, sizeof(int) * (size_t)std::max(nb, 64), s), "counters");
+  P.colsum = static_cast<double*>(ctx->buf[bl_ctx::B_COLSUM].ensure(sizeof(double) * bl::S_COUNT * (size_t)Kp));
+  bl::launch_spmm(P, s, transpose, tin, tout, active);
+  bl::launch_from_tiled(s, tout, raw, rout, width, W, active);
+  ck(cudaMemcpyAsync(out, raw, sizeof(double) * (size_t)rout * active, cudaMemcpyDeviceToHost, s), "out");
+  ck(cudaStreamSynchronize(s), "spmm sync");
+  ck(cudaGetLastError(), "spmm");
+}
+}  // namespace
+
 extern "C" {
 
 void bl_config_default(bl_config* c) {
@@ -1134,6 +1181,7 @@ void bl_ctx_destroy(bl_ctx* ctx) {
   free_tail_graph(ctx);
   if (ctx->pi_exec) cudaGraphExecDestroy(ctx->pi_exec);
   for (auto& b : ctx->buf) b.release();
+  for (DevBuf* b : {&ctx->csr_scratch.rp, &ctx->csr_scratch.ci, &ctx->csr_scratch.cv}) b->release();
   if (ctx->h_ctrl) cudaFreeHost(ctx->h_ctrl);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -1234,42 +1282,35 @@ int bl_spmm(bl_ctx* ctx, const bl_problem* p, int transpose, int32_t width,
             int32_t active, const double* x, double* out) {
   return guarded(ctx, [&] {
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-    if (active < 0) active = width;
-    if (active > width) raise(BL_ERR_INVALID_ARGUMENT, "spmm: active width too large");
-    if (active == 0) return;
-    const int rin = transpose ? p->m : p->n, rout = transpose ? p->n : p->m;
-    const int W = pow2_width(width);
-    const int Kp = (width + W - 1) / W * W;
+    device_spmm(ctx, p, transpose != 0, width, active, x, out);
+  });
+}
+
+int bl_csr_apply(bl_ctx* ctx, int32_t rows, int32_t cols, int64_t nnz, const int32_t* rowptr,
+                 const int32_t* col, const double* val, const double* x, double* out) {
+  return guarded(ctx, [&] {
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (rows < 0 || cols < 0 || nnz < 0) raise(BL_ERR_INVALID_ARGUMENT, "csr_apply: negative dimension");
+    if (nnz > INT32_MAX) raise(BL_ERR_INVALID_ARGUMENT, "csr_apply: too many nonzeros");
+    if (rows == 0) return;
+    if (rowptr[0] != 0 || rowptr[rows] != nnz)
+      raise(BL_ERR_INVALID_ARGUMENT, "csr_apply: malformed row offsets");
+    for (int32_t i = 0; i < rows; ++i)
+      if (rowptr[i + 1] < rowptr[i]) raise(BL_ERR_INVALID_ARGUMENT, "csr_apply: malformed row offsets");
+    for (int64_t q = 0; q < nnz; ++q)
+      if (col[q] < 0 || col[q] >= cols) raise(BL_ERR_OUT_OF_RANGE, "csr_apply: column index out of range");
+    // a transient one-orientation problem (grow-only buffers of the context)
+    bl_problem& t = ctx->csr_scratch;
     cudaStream_t s = ctx->stream;
-    double* tin = static_cast<double*>(ctx->buf[bl_ctx::B_TMP0].ensure(sizeof(double) * ((size_t)rin * Kp + 1)));
-    double* tout = static_cast<double*>(ctx->buf[bl_ctx::B_TMP1].ensure(sizeof(double) * ((size_t)rout * Kp + 1)));
-    double* raw = static_cast<double*>(ctx->buf[bl_ctx::B_WARMX].ensure(
-        sizeof(double) * ((size_t)std::max(rin, rout) * width + 1)));
-    ck(cudaMemcpyAsync(raw, x, sizeof(double) * (size_t)rin * active, cudaMemcpyHostToDevice, s), "x");
-    bl::launch_to_tiled(s, raw, tin, rin, width, W, active);
-    bl::Params P{};
-    P.m = p->m;
-    P.n = p->n;
-    P.rp = p->rp.as<int>();
-    P.ci = p->ci.as<int>();
-    P.cv = p->cv.as<double>();
-    P.trp = p->trp.as<int>();
-    P.tci = p->tci.as<int>();
-    P.tcv = p->tcv.as<double>();
-    P.W = W;
-    P.Kp = Kp;
-    P.grid = ctx->grid;
-    const int nb = Kp / W;
-    const int R = items_for(rout, W, ctx->grid);
-    P.partials = static_cast<double*>(ctx->buf[bl_ctx::B_PART].ensure(sizeof(double) * (size_t)nb * R * 10 * W));
-    P.counters = static_cast<int*>(ctx->buf[bl_ctx::B_CNT].ensure(sizeof(int) * (size_t)std::max(nb, 64)));
-    ck(cudaMemsetAsync(P.counters, 0, sizeof(int) * (size_t)std::max(nb, 64), s), "counters");
-    P.colsum = static_cast<double*>(ctx->buf[bl_ctx::B_COLSUM].ensure(sizeof(double) * bl::S_COUNT * (size_t)Kp));
-    bl::launch_spmm(P, s, transpose != 0, tin, tout, active);
-    bl::launch_from_tiled(s, tout, raw, rout, width, W, active);
-    ck(cudaMemcpyAsync(out, raw, sizeof(double) * (size_t)rout * active, cudaMemcpyDeviceToHost, s), "out");
-    ck(cudaStreamSynchronize(s), "spmm sync");
-    ck(cudaGetLastError(), "spmm");
+    t.ctx = ctx;
+    t.m = rows;
+    t.n = cols;
+    t.nnz = nnz;
+    upload(t.rp, rowptr, (size_t)rows + 1, s);
+    upload(t.ci, col, (size_t)nnz, s);
+    upload(t.cv, val, (size_t)nnz, s);
+    t.norm_valid = false;
+    device_spmm(ctx, &t, false, 1, 1, x, out);
   });
 }
 

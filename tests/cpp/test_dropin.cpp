@@ -93,6 +93,11 @@ int obbt_c2() {
   const ObbtOutcome o = run_obbt(p, cfg);
   std::printf("obbt changed %d solved %d limit %d\n", o.changed_count, o.solved_count,
               o.limit_count);
+  // every variable's tightened box (compared with the reference's run_obbt)
+  for (const ObbtVariable& v : o.variables)
+    std::printf("%d %d %a %d %a %d %d\n", v.variable, v.lower_changed ? 1 : 0, v.new_lower,
+                v.upper_changed ? 1 : 0, v.new_upper, static_cast<int>(v.lower_status),
+                static_cast<int>(v.upper_status));
   return 0;
 }
 

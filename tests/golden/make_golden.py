@@ -104,6 +104,28 @@ def c2():
         "seconds": time.time() - t, "threads": os.environ.get("BATCHLP_THREADS", "1")})
 
 
+def c2_bounds():
+    """The reference run_obbt (obbt.hpp:156-223) on C2: every tightened
+    bound, its change flag, margin and status, and the counts."""
+    p = I.config_problem("c2")
+    t = time.time()
+    o = ref.run_obbt(p)
+    write("c2_obbt_bounds.json", {
+        "source": "reference run_obbt, ObbtConfig{} (eps_opt 1e-4, eps_dual 1e-8, "
+                  "min_improvement 1e-4)",
+        "instance": "bl_gen_boxed_feasible(2000, 2000, 10, 11)",
+        "changed_count": o["changed_count"], "solved_count": o["solved_count"],
+        "limit_count": o["limit_count"], "iterations": o["iterations"],
+        "mean_reduction_pct": hx(o["mean_reduction_pct"]),
+        "new_lower": [hx(v) for v in o["new_lower"]],
+        "new_upper": [hx(v) for v in o["new_upper"]],
+        "lower_changed": o["lower_changed"].tolist(),
+        "upper_changed": o["upper_changed"].tolist(),
+        "lower_status": o["lower_status"].tolist(),
+        "upper_status": o["upper_status"].tolist(),
+        "seconds": time.time() - t, "threads": os.environ.get("BATCHLP_THREADS", "1")})
+
+
 if __name__ == "__main__":
     os.environ.setdefault("BATCHLP_THREADS", str(os.cpu_count() or 1))
     which = sys.argv[1:] or ["tiny", "spectral", "c1", "c2"]

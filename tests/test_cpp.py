@@ -1,11 +1,16 @@
 """The C++ drop-in (include/batchlp/*.hpp over libbatchlp_cuda.so).
 
 * The reference's OWN unit suites (test_bounds, test_sparse, test_problem,
-  test_batch_solver, test_strong_branching, test_obbt, test_tuner, test_mps,
+  test_solver, test_batch_solver, test_strong_branching, test_obbt, test_tuner, test_mps,
   test_generators), compiled unmodified against our headers by
   tests/cpp/Makefile, pass on the B200 (test_mps / test_generators exercise
   the reference's own host-side MPS reader and generators over our problem
   types).
+* The reference's acceptance driver (tests/acceptance.cpp, criteria 1-10:
+  oracle equivalence on 500 LPs, width-one batch = single solve, batched
+  FSB vs per-branch oracles, OBBT safety, certificates, restarts, the
+  residual metric, throughput trend, MPS round trip), compiled unmodified
+  against our headers, passes on the B200.
 * Our C++ API tests (tests/cpp/test_dropin.cpp) pass on the B200.
 * C1 strong branching and C2 OBBT through the C++ API match the reference's
   golden results (status identical, objective 1e-6 relative, iterations 10 %).
@@ -22,6 +27,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "tests", "cpp", "_build")
 REF_SUITES = os.path.join(BUILD, "ref_suites")
 DROPIN = os.path.join(BUILD, "dropin_tests")
+ACCEPT = os.path.join(BUILD, "acceptance")
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 
@@ -66,6 +72,16 @@ def test_reference_suites_pass_on_device():
     r = _run([REF_SUITES])
     assert r.returncode == 0, (r.stdout + r.stderr)[-6000:]
     assert " 0 failed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_criteria_pass_on_device(tmp_path):
+    _require(ACCEPT)
+    # acceptance.cpp writes tune_report.csv into its working directory
+    r = subprocess.run([ACCEPT], capture_output=True, text=True, timeout=1200, cwd=tmp_path)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-6000:]
+    assert out.count("[PASS]") == 10, out[-6000:]
 
 
 @pytest.mark.gpu
@@ -123,3 +139,18 @@ def test_cpp_obbt_c2_matches_reference_golden():
         assert _close(float.fromhex(ob), float.fromhex(want["objective"]), 1e-6)
     tail = lines[1 + len(cols)].split()
     assert tail[0] == "obbt" and int(tail[6]) + int(tail[4]) == len(cols)
+    # run_obbt's tightened boxes against the reference's run_obbt
+    # (obbt.hpp:156-223; tests/golden/c2_obbt_bounds.json)
+    with open(os.path.join(GOLDEN, "c2_obbt_bounds.json")) as f:
+        gb = json.load(f)
+    assert int(tail[2]) == gb["changed_count"]
+    assert int(tail[4]) == gb["solved_count"] and int(tail[6]) == gb["limit_count"]
+    rows = lines[2 + len(cols):]
+    assert len(rows) == len(gb["new_lower"])
+    for i, ln in enumerate(rows):
+        var, lc, nl, uc, nu, ls, us = ln.split()
+        assert int(var) == i
+        assert (int(lc), int(uc)) == (gb["lower_changed"][i], gb["upper_changed"][i]), i
+        assert (int(ls), int(us)) == (gb["lower_status"][i], gb["upper_status"][i]), i
+        assert _close(float.fromhex(nl), float.fromhex(gb["new_lower"][i]), 1e-6), i
+        assert _close(float.fromhex(nu), float.fromhex(gb["new_upper"][i]), 1e-6), i
