@@ -67,6 +67,13 @@ enum class VectorMode {
 
 struct BatchOptions {
   VectorMode vectors = VectorMode::kCertificate;
+  // Multi-GPU (extension): two or more device ordinals shard
+  // the batch into contiguous column slices, one per listed device (a device
+  // listed twice gets two contexts); A is replicated, nothing is exchanged
+  // while iterating, and each slice restarts on its own averaged residual
+  // -- the result equals the reference's solve_batch run slice by slice.
+  // Empty or one entry: the workspace's (or this thread's) context.
+  std::vector<int> devices;
 };
 
 inline BatchSolveSummary solve_batch(const BatchProblem& batch, const SolverConfig& cfg = {},
@@ -94,9 +101,23 @@ inline BatchSolveSummary solve_batch(const BatchProblem& batch, const SolverConf
   if (!initial_weights.empty() && static_cast<int>(initial_weights.size()) != width)
     throw std::invalid_argument("solve_batch: initial weight count mismatch");
 
-  cuda::Context& ctx = external_ws ? external_ws->context() : cuda::thread_context();
-  detail::DeviceRun run = detail::run_on_device(ctx, batch, cfg, cols, initial_weights, nullptr,
-                                                static_cast<int>(options.vectors));
+  detail::DeviceRun run;
+  if (options.devices.size() > 1) {
+    std::vector<cuda::Context*> ctxs;
+    for (std::size_t k = 0; k < options.devices.size(); ++k) {
+      int seen = 0;
+      for (std::size_t q = 0; q < k; ++q) seen += options.devices[q] == options.devices[k];
+      ctxs.push_back(&cuda::shard_context(options.devices[k], seen));
+    }
+    run = detail::run_sharded(ctxs, batch, cfg, cols, initial_weights,
+                              static_cast<int>(options.vectors));
+  } else {
+    cuda::Context& ctx = external_ws           ? external_ws->context()
+                         : options.devices.empty() ? cuda::thread_context()
+                                                   : cuda::shard_context(options.devices[0], 0);
+    run = detail::run_on_device(ctx, batch, cfg, cols, initial_weights, nullptr,
+                                static_cast<int>(options.vectors));
+  }
   summary.iterations = run.summary.iterations;
   summary.restarts = run.summary.restarts;
   summary.sparse_products = run.summary.sparse_products;

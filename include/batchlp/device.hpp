@@ -23,6 +23,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "batchlp/detail/csr.hpp"
@@ -147,6 +148,19 @@ inline Context& thread_context() {
   thread_local std::unique_ptr<Context> ctx;
   if (!ctx) ctx = std::make_unique<Context>();
   return *ctx;
+}
+
+// Contexts of a sharded solve (BatchOptions::devices): one per (device,
+// occurrence) on this host thread, so a device listed twice gets two
+// independent contexts (two streams on one GPU).
+inline Context& shard_context(int device, int occurrence) {
+  thread_local std::vector<std::unique_ptr<Context>> pool;
+  thread_local std::vector<std::pair<int, int>> keys;
+  for (std::size_t k = 0; k < keys.size(); ++k)
+    if (keys[k] == std::pair<int, int>{device, occurrence}) return *pool[k];
+  pool.push_back(std::make_unique<Context>(device));
+  keys.emplace_back(device, occurrence);
+  return *pool.back();
 }
 
 }  // namespace batchlp::cuda

@@ -239,6 +239,32 @@ int bl_solve_batch(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
                    const double* warm_x, const double* warm_y,
                    bl_summary* summary, bl_column_result* results);
 
+/* ---- multi-GPU: the batch sharded across devices ----------
+ * One (context, problem) pair per shard -- normally one per GPU, each with
+ * its own replica of A uploaded by bl_problem_upload on that context. The
+ * width LPs are split into n_shards contiguous near-equal column slices
+ * (shard s: [s*width/G ...), the first width % G slices one longer); each
+ * shard runs bl_solve_batch on its slice on its own host thread, with no
+ * communication while iterating (restarts synchronise on the SLICE's
+ * averaged residual, i.e. this is exactly n_shards reference solve_batch
+ * runs on the slices, the parity definition of SURVEY §8(e)). Overrides,
+ * presets and initial weights are given for the whole batch (original
+ * column indices) and routed to their shard; signed-unit batches stay
+ * signed-unit per slice. Every shard copies its per-LP records straight
+ * into its slice of `results` (original column order): the gather is one
+ * device-to-host copy per GPU, nothing crosses between devices.
+ * summaries: NULL or n_shards entries (per-shard iterations, restarts, eta,
+ * device time). Vectors of shard s are fetched from ctxs[s] with the
+ * column index local to its slice. Errors: the whole-batch checks come
+ * first (codes as bl_solve_batch); a shard's failure is reported as
+ * "shard s: ..." with that shard's code on ctxs[0]. */
+int bl_solve_batch_sharded(bl_ctx* const* ctxs, bl_problem* const* probs, int32_t n_shards,
+                           int32_t width, int32_t mode, const bl_override* overrides,
+                           int32_t n_overrides, const bl_config* cfg,
+                           const int32_t* preset_columns, int32_t n_presets,
+                           const double* initial_weights, bl_summary* summaries,
+                           bl_column_result* results);
+
 /* Vectors of the last solve on this context (lazy copy-back). */
 int bl_fetch_solution(bl_ctx* ctx, int32_t column, double* x, double* y,
                       double* reduced);

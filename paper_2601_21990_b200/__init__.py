@@ -11,8 +11,8 @@ from .problem import (BatchProblem, Bounds, ColumnOverride, ColumnView, Interval
                       kInf, make_problem, resolve_column, validate)
 from .solver import (BatchSolveSummary, BatchWorkspace, InfeasibilityProbe, PresetColumn,
                      Residuals, RestartEvent, RestartReason, SolveResult, SolverConfig,
-                     SolveStatus, Vectors, WarmStart, solve, solve_batch, spectral_norm, spmm,
-                     spmv, step_size_for)
+                     SolveStatus, Vectors, WarmStart, solve, solve_batch, solve_batch_sharded,
+                     spectral_norm, spmm, spmv, step_size_for)
 from .drivers import (FsbBranch, FsbDriver, FsbOutcome, FsbRequest, ObbtConfig, ObbtOutcome,
                       ObbtVariable, build_fsb_batch, build_obbt_batch, certified_value,
                       run_fsb, run_obbt, score_branching)

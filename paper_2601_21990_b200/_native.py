@@ -157,6 +157,11 @@ SIGNATURES = {
     "bl_csr_apply": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int64, _IP, _IP, _DP, _DP, _DP]),
     "bl_measure_spmm": (C.c_int, [_P, _P, C.c_int32, C.c_int32, _DP, _DP,
                                   C.POINTER(C.c_int32)]),
+    "bl_solve_batch_sharded": (
+        C.c_int,
+        [C.POINTER(_P), C.POINTER(_P), C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, _P,
+         _IP, C.c_int32, _DP, _P, _P],
+    ),
     "bl_solve_batch": (
         C.c_int,
         [_P, _P, C.c_int32, C.c_int32, C.POINTER(bl_override), C.c_int32,

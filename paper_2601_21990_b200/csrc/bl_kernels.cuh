@@ -472,8 +472,8 @@ __device__ __forceinline__ void col_vals(const Params& P, const ColInfo& c, int 
   lo = bl;
   hi = bh;
   if (P.mode == BL_SIGNED_UNIT_COLUMNS) {
-    const int n = P.n;
-    cc = c.orig < n ? (i == c.orig ? 1.0 : 0.0) : (i == c.orig - n ? -1.0 : 0.0);
+    const int n = P.n, o = c.orig + P.unit_off;
+    cc = o < n ? (i == o ? 1.0 : 0.0) : (i == o - n ? -1.0 : 0.0);
   }
   if (c.v0 == i) apply_ov(c.k0, c.val0, cc, lo, hi);
   for (int k = c.ob + 1; k < c.oe; ++k)
@@ -1174,12 +1174,27 @@ static __device__ void permute_slots(const Params& P, const int* perm, int width
   }
 }
 
+// Diagnostic timing of decide_body on plain passes (P.dbg slots 10-14).
+static __device__ __noinline__ unsigned long long* decide_mark_slot() {
+  __shared__ unsigned long long t;
+  return &t;
+}
+__device__ __forceinline__ void decide_mark(const Params& P, bool plain, int k) {
+  if (P.dbg && threadIdx.x == 0 && plain) {
+    const unsigned long long now = gtime();
+    if (k > 10) P.dbg[k] += now - *decide_mark_slot();
+    else P.dbg[10] += 1;
+    *decide_mark_slot() = now;
+  }
+}
+
 // Everything after the per-column verdicts (batch_solver.hpp:229-338).
 static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* sh,
                          int* ish, double* scratch) {
   const int tid = threadIdx.x;
   const int active0 = C.active;
   const int width = P.width;
+  const bool plain = !C.check;
   int* snap_bits = P.cert_flag;  // reused: cert flags are consumed by now
   __shared__ int n_fin, n_snap;
   if (tid == 0) {
@@ -1224,6 +1239,7 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
     }
   }
   __syncthreads();
+  decide_mark(P, plain, 16);
   int active = active0;
   int* perm = P.move_src;
   const bool at_cap = C.at_cap;
@@ -1277,6 +1293,7 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
     permute_slots(P, perm, width, scratch);
     if (tid == 0) C.col_epoch += 1;
   }
+  decide_mark(P, plain, 17);
   // iteration limit: freeze what is left from the best candidates (:280-295)
   if (at_cap && active > 0) {
     for (int j = tid; j < active; j += (int)blockDim.x) {
@@ -1304,6 +1321,7 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
     }
     __syncthreads();
   }
+  decide_mark(P, plain, 18);
   // snapshot list (pre-compaction slots) and move list (post <- pre)
   if (C.check) {
     for (int j = tid; j < active0; j += (int)blockDim.x) {
@@ -1332,6 +1350,7 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
     n_moves = ish[1];
   }
   __syncthreads();
+  decide_mark(P, plain, 19);
 
   if (tid == 0) {
     C.n_snap = n_snap;
@@ -1364,6 +1383,7 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
     }
   }
   __syncthreads();
+  decide_mark(P, plain, 20);
   const bool restart = ish[2] != 0;
   if (restart) {
     // gated weight update on the post-compaction active columns (:303-319)
@@ -1376,6 +1396,7 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
     }
   }
   __syncthreads();
+  decide_mark(P, plain, 21);
   if (tid == 0) {
     C.hash_pending = 0;
     if (!C.done) {
@@ -1414,6 +1435,7 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
     set_cond(P, P.h_snap, (C.n_snap > 0 || C.n_moves > 0) ? 1u : 0u);
     if (P.trace) set_cond(P, P.h_trace, C.hash_pending ? 1u : 0u);
   }
+  decide_mark(P, plain, 22);
 }
 
 // Folds the finished launches' entry/exit stamps into the accumulators and
@@ -1436,20 +1458,6 @@ static __device__ void prof_fold(const Params& P, const Ctrl& C, int k, unsigned
   P.prof_acc[3 * K_DUAL + 2] += 12.0 * nnz + 4.0 * (m + 1) + 16.0 * m + 8.0 * K * (n + 6.0 * m + chk * 3.0 * m);
   if (C.check)
     P.prof_acc[3 * K_CHECK + 2] += 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 5.0 * n);
-}
-
-// Diagnostic timing of decide_body on plain passes (P.dbg slots 10-14).
-static __device__ __noinline__ unsigned long long* decide_mark_slot() {
-  __shared__ unsigned long long t;
-  return &t;
-}
-__device__ __forceinline__ void decide_mark(const Params& P, bool plain, int k) {
-  if (P.dbg && threadIdx.x == 0 && plain) {
-    const unsigned long long now = gtime();
-    if (k > 10) P.dbg[k] += now - *decide_mark_slot();
-    else P.dbg[10] += 1;
-    *decide_mark_slot() = now;
-  }
 }
 
 static __device__ void decide_body(const Params& P, int phase) {

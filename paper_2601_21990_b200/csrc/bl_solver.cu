@@ -24,6 +24,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "batchlp_cuda.h"
@@ -566,12 +567,13 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
                       const bl_override* ov, int32_t n_ov, const bl_config* cfg_in,
                       const int32_t* presets, int32_t n_presets, const double* w0,
                       const double* warm_x, const double* warm_y, bl_summary* summary,
-                      bl_column_result* results) {
+                      bl_column_result* results, int unit_off = -1) {
   const bl_config cfg = config_or_default(cfg_in);
   const int n = p->n, m = p->m;
-  // BatchProblem constructor checks (problem.hpp:146-167)
+  // BatchProblem constructor checks (problem.hpp:146-167); a shard of a
+  // signed-unit batch (unit_off >= 0) was checked as a whole by the caller
   if (width < 0) raise(BL_ERR_INVALID_ARGUMENT, "batch: negative width");
-  if (mode == BL_SIGNED_UNIT_COLUMNS && width != 2 * n)
+  if (mode == BL_SIGNED_UNIT_COLUMNS && unit_off < 0 && width != 2 * n)
     raise(BL_ERR_INVALID_ARGUMENT, "batch: signed unit columns require width 2n");
   for (int k = 0; k < n_ov; ++k) {
     const bl_override& o = ov[k];
@@ -668,6 +670,7 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.width = width;
   P.Kp = Kp;
   P.mode = mode;
+  P.unit_off = unit_off > 0 ? unit_off : 0;
   P.W = W;
   P.X[0] = dmat(bl_ctx::B_X0, n);
   P.X[1] = dmat(bl_ctx::B_X1, n);
@@ -892,8 +895,8 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.dbg = nullptr;
   if (std::getenv("BATCHLP_TAIL_TRACE")) {
     P.dbg = static_cast<unsigned long long*>(
-        ctx->buf[bl_ctx::B_DBG].ensure(sizeof(unsigned long long) * 16));
-    ck(cudaMemsetAsync(P.dbg, 0, sizeof(unsigned long long) * 16, s), "dbg");
+        ctx->buf[bl_ctx::B_DBG].ensure(sizeof(unsigned long long) * 32));
+    ck(cudaMemsetAsync(P.dbg, 0, sizeof(unsigned long long) * 32, s), "dbg");
   }
   P.barrier = static_cast<unsigned long long*>(
       ctx->buf[bl_ctx::B_BAR].ensure(sizeof(unsigned long long)));
@@ -1003,7 +1006,7 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   ck(cudaEventRecord(ctx->ev1, s), "event");
   ck(cudaStreamSynchronize(s), "solve sync");
   if (P.dbg) {
-    unsigned long long d[16];
+    unsigned long long d[32];
     cudaMemcpy(d, P.dbg, sizeof(d), cudaMemcpyDeviceToHost);
     const double passes = d[0] > 0 ? (double)d[0] : 1.0;
     static const char* what[] = {"", "top->rows", "primal rows", "primal publish", "primal sync",
@@ -1016,6 +1019,10 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
     std::fprintf(stderr, "[decide trace] %llu plain passes\n", (unsigned long long)d[10]);
     for (int k = 11; k < 14; ++k)
       std::fprintf(stderr, "[decide trace] %-16s %8.3f us/pass\n", dwhat[k - 11], d[k] / dp / 1e3);
+    static const char* fwhat[] = {"fin: verdicts", "fin: compaction", "fin: cap", "fin: lists",
+                                  "fin: rule+geometry", "fin: weights", "fin: conds"};
+    for (int k = 16; k < 23; ++k)
+      std::fprintf(stderr, "[decide trace] %-18s %8.3f us/pass\n", fwhat[k - 16], d[k] / dp / 1e3);
     std::fprintf(stderr, "[fast decide] ctrl+fold+resid %8.3f us/pass\n", d[14] / passes / 1e3);
     std::fprintf(stderr, "[fast decide] mean+rule       %8.3f us/pass\n", d[15] / passes / 1e3);
   }
@@ -1401,6 +1408,102 @@ int bl_solve_batch(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
     solve_batch_impl(ctx, p, width, mode, overrides, n_overrides, cfg, preset_columns,
                      n_presets, initial_weights, warm_x, warm_y, summary, results);
+  });
+}
+
+int bl_solve_batch_sharded(bl_ctx* const* ctxs, bl_problem* const* probs, int32_t n_shards,
+                           int32_t width, int32_t mode, const bl_override* overrides,
+                           int32_t n_overrides, const bl_config* cfg,
+                           const int32_t* preset_columns, int32_t n_presets,
+                           const double* initial_weights, bl_summary* summaries,
+                           bl_column_result* results) {
+  if (n_shards < 1 || ctxs == nullptr || probs == nullptr) {
+    g_create_error = "solve_batch_sharded: need at least one (context, problem) pair";
+    return BL_ERR_INVALID_ARGUMENT;
+  }
+  bl_ctx* lead = ctxs[0];
+  return guarded(lead, [&] {
+    for (int s = 0; s < n_shards; ++s) {
+      if (!ctxs[s] || !probs[s] || probs[s]->ctx != ctxs[s])
+        raise(BL_ERR_INVALID_ARGUMENT, "solve_batch_sharded: problem of another context");
+      for (int t = 0; t < s; ++t)
+        if (ctxs[t] == ctxs[s])
+          raise(BL_ERR_INVALID_ARGUMENT, "solve_batch_sharded: a context appears twice");
+      if (probs[s]->m != probs[0]->m || probs[s]->n != probs[0]->n ||
+          probs[s]->nnz != probs[0]->nnz)
+        raise(BL_ERR_INVALID_ARGUMENT, "solve_batch_sharded: replicas of different problems");
+    }
+    const int n = probs[0]->n;
+    // the whole batch's checks, in the single-device order (problem.hpp:146-167,
+    // solver.hpp:90-102, batch_solver.hpp:93-99); each shard re-checks its part
+    if (width < 0) raise(BL_ERR_INVALID_ARGUMENT, "batch: negative width");
+    if (mode == BL_SIGNED_UNIT_COLUMNS && width != 2 * n)
+      raise(BL_ERR_INVALID_ARGUMENT, "batch: signed unit columns require width 2n");
+    for (int k = 0; k < n_overrides; ++k)
+      if (overrides[k].column < 0 || overrides[k].column >= width)
+        raise(BL_ERR_OUT_OF_RANGE, "batch: override column out of range");
+    check_config(config_or_default(cfg));
+    std::vector<char> seen(width > 0 ? width : 0, 0);
+    for (int k = 0; k < n_presets; ++k) {
+      const int c = preset_columns[k];
+      if (c < 0 || c >= width) raise(BL_ERR_OUT_OF_RANGE, "solve_batch: preset column out of range");
+      if (seen[c]) raise(BL_ERR_INVALID_ARGUMENT, "solve_batch: duplicate preset column");
+      seen[c] = 1;
+    }
+    // contiguous near-equal column slices (distributed.py column_slices)
+    std::vector<int> beg(n_shards + 1, 0);
+    for (int s = 0, at = 0; s < n_shards; ++s) {
+      beg[s] = at;
+      at += width / n_shards + (s < width % n_shards ? 1 : 0);
+      beg[s + 1] = at;
+    }
+    struct Part {
+      std::vector<bl_override> ov;
+      std::vector<int32_t> presets;
+      std::vector<double> w0;
+      int code = BL_OK;
+      std::string msg;
+    };
+    std::vector<Part> parts(n_shards);
+    for (int k = 0; k < n_overrides; ++k) {  // overrides keep their list order
+      const int c = overrides[k].column;
+      const int s = int(std::upper_bound(beg.begin(), beg.end() - 1, c) - beg.begin()) - 1;
+      bl_override o = overrides[k];
+      o.column = c - beg[s];
+      parts[s].ov.push_back(o);
+    }
+    for (int k = 0; k < n_presets; ++k) {
+      const int c = preset_columns[k];
+      const int s = int(std::upper_bound(beg.begin(), beg.end() - 1, c) - beg.begin()) - 1;
+      parts[s].presets.push_back(c - beg[s]);
+    }
+    // one host thread per shard, each on its own context / device; every
+    // shard writes its per-LP records straight into its slice of `results`
+    auto run = [&](int s) {
+      Part& pt = parts[s];
+      bl_ctx* c = ctxs[s];
+      const int w = beg[s + 1] - beg[s];
+      const int rc = guarded(c, [&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        solve_batch_impl(c, probs[s], w, mode, pt.ov.data(), (int32_t)pt.ov.size(), cfg,
+                         pt.presets.empty() ? nullptr : pt.presets.data(),
+                         (int32_t)pt.presets.size(),
+                         initial_weights ? initial_weights + beg[s] : nullptr, nullptr, nullptr,
+                         summaries ? &summaries[s] : nullptr, results + beg[s],
+                         mode == BL_SIGNED_UNIT_COLUMNS ? beg[s] : -1);
+      });
+      if (rc != BL_OK) {
+        pt.code = rc;
+        pt.msg = c->err;
+      }
+    };
+    std::vector<std::thread> threads;
+    for (int s = 1; s < n_shards; ++s) threads.emplace_back(run, s);
+    run(0);
+    for (std::thread& t : threads) t.join();
+    for (int s = 0; s < n_shards; ++s)
+      if (parts[s].code != BL_OK)
+        raise(parts[s].code, "shard " + std::to_string(s) + ": " + parts[s].msg);
   });
 }
 

@@ -186,6 +186,7 @@ class BatchSolveSummary:
     kernel_launches: int = 0
     loop_passes: int = 0
     profile: Dict[str, tuple] = field(default_factory=dict)  # kind -> (launches, ns, bytes)
+    shards: List[dict] = field(default_factory=list)  # per-shard scalars (sharded solves)
 
 
 # ---------------------------------------------------------------------------
@@ -483,6 +484,67 @@ def solve_batch(batch: BatchProblem, cfg: Optional[SolverConfig] = None,
             else:
                 r.certificate = InfeasibilityProbe(dx, np.zeros(0), np.zeros(0))
         out.per_problem.append(r)
+    return out
+
+
+def solve_batch_sharded(batch: BatchProblem, cfg: Optional[SolverConfig] = None,
+                        presets: Sequence[PresetColumn] = (),
+                        workspaces: Sequence[BatchWorkspace] = (),
+                        initial_weights: Optional[Sequence[float]] = None, *,
+                        vectors: int = Vectors.NONE) -> BatchSolveSummary:
+    """The batch sharded over several device contexts in one process
+    (bl_solve_batch_sharded): one workspace per shard --
+    normally one per GPU -- each holding a replica of the problem and solving
+    one contiguous column slice with no exchange while iterating. Results are
+    in original column order; the summary merges the shards (iterations of
+    the longest, restarts / products summed, restart logs concatenated).
+    Equals the reference's solve_batch run slice by slice."""
+    cfg = cfg or SolverConfig()
+    if len(workspaces) < 1:
+        raise InvalidArgument("solve_batch_sharded: need at least one workspace")
+    L = N.lib()
+    width = batch.batch_width()
+    base = batch.base()
+    G = len(workspaces)
+    dps = [ws.resident(base) for ws in workspaces]
+    ctxs = (C.c_void_p * G)(*[ws.ctx.handle for ws in workspaces])
+    probs = (C.c_void_p * G)(*[dp.handle for dp in dps])
+    ovs = batch.overrides()
+    ov_arr = (N.bl_override * max(len(ovs), 1))()
+    for k, o in enumerate(ovs):
+        ov_arr[k].column, ov_arr[k].kind = o.column, int(o.kind)
+        ov_arr[k].variable, ov_arr[k].value = o.variable, o.value
+    pcols = np.array([q.column for q in presets], dtype=np.int32)
+    w0 = None
+    if initial_weights is not None and len(initial_weights) > 0:
+        if len(initial_weights) != width:
+            raise InvalidArgument("solve_batch: initial weight count mismatch")
+        w0 = np.ascontiguousarray(initial_weights, dtype=np.float64)
+    ccfg = cfg.to_c(vectors)
+    sums = (N.bl_summary * G)()
+    res = (N.bl_column_result * max(width, 1))()
+    _check(workspaces[0].ctx.handle, L.bl_solve_batch_sharded(
+        ctxs, probs, G, width, int(batch.objective_mode()), C.cast(ov_arr, C.c_void_p),
+        len(ovs), C.cast(C.pointer(ccfg), C.c_void_p),
+        N.iptr(pcols) if len(pcols) else None, len(pcols), N.dptr(w0),
+        C.cast(sums, C.c_void_p), C.cast(res, C.c_void_p)))
+    out = BatchSolveSummary()
+    for q in sums:
+        out.iterations = max(out.iterations, int(q.iterations))
+        out.restarts += int(q.restarts)
+        out.sparse_products += int(q.sparse_products)
+        out.device_ms = max(out.device_ms, q.device_ms)
+        out.kernel_launches += int(q.kernel_launches)
+        out.loop_passes = max(out.loop_passes, int(q.loop_passes))
+        out.eta = q.eta
+        out.shards.append({"iterations": int(q.iterations), "restarts": int(q.restarts),
+                           "device_ms": q.device_ms, "loop_passes": int(q.loop_passes)})
+    if width == 0:
+        return out
+    preset_of = {q.column: q for q in presets}
+    converted = _results_from_c(res, width)
+    out.per_problem = [preset_of[j].result if j in preset_of else converted[j]
+                       for j in range(width)]
     return out
 
 

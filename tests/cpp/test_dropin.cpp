@@ -177,6 +177,49 @@ TEST_CASE("sparse products match a hand product") {
   CHECK(yt.at(1, 0) == 6.0);
 }
 
+TEST_CASE("a batch sharded over two contexts equals its slices solved one by one") {
+  // OBBT on a small boxed LP: a signed-unit batch of 2n columns, split in two
+  // contiguous slices (BatchOptions::devices = {0, 0}: two contexts, one GPU)
+  bl_instance in{};
+  REQUIRE(bl_gen_boxed_feasible(120, 150, 6, 3, &in) == 0);
+  const LpProblem p = from_instance(in);
+  ObbtConfig ocfg;
+  const ObbtBatch built = build_obbt_batch(p, ocfg);
+  BatchOptions two;
+  two.vectors = VectorMode::kSolution;
+  two.devices = {0, 0};
+  const BatchSolveSummary whole =
+      solve_batch(built.batch, ocfg.solver_config(), built.presets, nullptr, {}, two);
+  const int width = built.batch.batch_width(), n = p.num_cols();
+  REQUIRE(static_cast<int>(whole.per_problem.size()) == width);
+  for (int half = 0; half < 2; ++half) {
+    const int b = half * (width / 2), e = b + width / 2;
+    // the slice as its own batch: signed units rewritten as objective entries
+    LpProblem zero = p;
+    zero.objective.assign(n, 0.0);
+    std::vector<ColumnOverride> ov;
+    for (int c = b; c < e; ++c)
+      ov.push_back(ColumnOverride{c - b, OverrideKind::kObjectiveEntry, c < n ? c : c - n,
+                                  c < n ? 1.0 : -1.0});
+    const BatchProblem slice(zero, e - b, ObjectiveMode::kSharedObjective, ov);
+    std::vector<PresetColumn> pre;
+    for (const PresetColumn& q : built.presets)
+      if (q.column >= b && q.column < e) pre.push_back(PresetColumn{q.column - b, q.result});
+    BatchOptions one;
+    one.vectors = VectorMode::kSolution;
+    const BatchSolveSummary s =
+        solve_batch(slice, ocfg.solver_config(), pre, nullptr, {}, one);
+    for (int j = 0; j < e - b; ++j) {
+      const SolveResult& g = whole.per_problem[b + j];
+      const SolveResult& w = s.per_problem[j];
+      CHECK(g.status == w.status);
+      CHECK(g.iterations == w.iterations);
+      CHECK(std::memcmp(&g.objective, &w.objective, sizeof(double)) == 0);
+      CHECK(g.x == w.x);
+    }
+  }
+}
+
 int main(int argc, char** argv) {
   if (argc > 2 && std::strcmp(argv[1], "--fsb-c1") == 0) return fsb_c1(argv[2]);
   if (argc > 1 && std::strcmp(argv[1], "--obbt-c2") == 0) return obbt_c2();

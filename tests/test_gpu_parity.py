@@ -142,3 +142,53 @@ def test_broken_step_size_raises_domain_error(ref, shape, seed, k):
         bl.solve_batch(batch, cfg, (), vectors=bl.Vectors.NONE, eta=eta)
     # the same solve at the reference's own step size is fine
     bl.solve_batch(batch, cfg, (), vectors=bl.Vectors.NONE)
+
+
+def _slices(width, g):
+    base, extra = divmod(width, g)
+    out, s = [], 0
+    for r in range(g):
+        e = s + base + (1 if r < extra else 0)
+        out.append((s, e))
+        s = e
+    return out
+
+
+def _sharded_case(kind):
+    if kind == "fsb":  # C1 strong branching (the reference's root point)
+        with open(os.path.join(GOLDEN, "c1_fsb.json")) as f:
+            g = json.load(f)
+        p = I.config_problem("c1")
+        x = np.array([float.fromhex(v) for v in g["x_rel"]])
+        fb = bl.build_fsb_batch(bl.FsbRequest(p, x, g["fractional"]))
+        return fb.batch, fb.presets, bl.SolverConfig()
+    p = I.boxed_feasible(300, 300, 10, 5)  # OBBT: a signed-unit batch of 600
+    ob = bl.build_obbt_batch(p, bl.ObbtConfig())
+    return ob.batch, ob.presets, bl.ObbtConfig().solver_config()
+
+
+@pytest.mark.parametrize("kind", ["fsb", "obbt"])
+def test_sharded_contexts_match_reference_slices(ref, kind):
+    """Two contexts on one B200 (bl_solve_batch_sharded):
+    every slice equals the reference's solve_batch on that slice, and is
+    bit-identical to a single-context device solve of the same slice (a
+    signed-unit slice is solved in place through the unit offset; the
+    single-context run gets it rewritten as objective-entry overrides)."""
+    import bench
+    batch, presets, cfg = _sharded_case(kind)
+    ws = [bl.BatchWorkspace(0), bl.BatchWorkspace(0)]
+    got = bl.solve_batch_sharded(batch, cfg, presets, ws)
+    assert len(got.per_problem) == batch.batch_width()
+    for b, e in _slices(batch.batch_width(), 2):
+        lp, sb, sp = bench.subset_batch(bl, batch, presets, list(range(b, e)))
+        want = ref.solve_batch(lp, sb.batch_width(), 0, sb.overrides(), cfg, _presets(sp),
+                               vectors=False)
+        one = bl.solve_batch(sb, cfg, sp, vectors=bl.Vectors.NONE)
+        sl = got.per_problem[b:e]
+        for j, (g, w, o) in enumerate(zip(sl, want.per_problem, one.per_problem)):
+            assert int(g.status) == w.status, (b, j)
+            assert abs(g.iterations - w.iterations) <= 0.1 * max(w.iterations, 1), (b, j)
+            if np.isfinite(w.objective):
+                assert abs(g.objective - w.objective) <= 1e-6 * (1 + abs(w.objective)), (b, j)
+            assert (int(g.status), g.iterations) == (int(o.status), o.iterations), (b, j)
+            assert g.objective == o.objective or (np.isnan(g.objective) and np.isnan(o.objective))
