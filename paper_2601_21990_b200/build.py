@@ -121,7 +121,16 @@ def build_cpp_tests(verbose: bool = False) -> None:
     subprocess.run(cmd, check=True)
 
 
+def build_tools(verbose: bool = False) -> None:
+    """tools/Makefile: the MPS command-line runner (tools/batchlp_run.cpp)."""
+    cmd = ["make", "-s", "-C", os.path.join(ROOT, "tools")]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+
+
 if __name__ == "__main__":
     build_library(force="--force" in sys.argv, verbose=True)
     build_oracles(verbose=True)
     build_cpp_tests(verbose=True)
+    build_tools(verbose=True)

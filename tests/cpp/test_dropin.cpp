@@ -8,10 +8,14 @@
 //                                     fixture); prints one line per branch
 //   dropin_tests --obbt-c2            C2 OBBT batch through solve_batch and
 //                                     run_obbt; prints one line per column
+//   dropin_tests --write-mps R C D S FILE
+//                                     generate_set_cover(R, C, D, S) written
+//                                     as MPS (all columns integral)
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -220,7 +224,44 @@ TEST_CASE("a batch sharded over two contexts equals its slices solved one by one
   }
 }
 
+int write_set_cover_mps(char** argv) {
+  bl_instance in{};
+  if (bl_gen_set_cover(std::atoi(argv[0]), std::atoi(argv[1]), std::atof(argv[2]),
+                       std::strtoull(argv[3], nullptr, 10), &in) != 0)
+    return 1;
+  const LpProblem p = from_instance(in);
+  std::vector<int> ints(static_cast<std::size_t>(p.num_cols()));
+  for (int c = 0; c < p.num_cols(); ++c) ints[c] = c;
+  std::ofstream out(argv[4]);
+  write_mps(out, p, ints, "setcover");
+  return out ? 0 : 1;
+}
+
+TEST_CASE("MPS round trip keeps every entry, bound and integrality mark") {
+  bl_instance in{};
+  REQUIRE(bl_gen_boxed_feasible(40, 50, 5, 9, &in) == 0);
+  const LpProblem p = from_instance(in);
+  std::ostringstream text;
+  write_mps(text, p, {1, 2, 7}, "boxed");
+  const MpsModel back = parse_mps_string(text.str());
+  CHECK(back.name == "boxed");
+  CHECK(back.integer_columns == std::vector<int>{1, 2, 7});
+  REQUIRE(back.problem.A.nnz() == p.A.nnz());
+  const CsrView a = p.A.view(), b = back.problem.A.view();
+  for (std::size_t q = 0; q < a.values.size(); ++q) {
+    CHECK(a.cols[q] == b.cols[q]);
+    CHECK(a.values[q] == b.values[q]);  // %.17g: exact
+  }
+  CHECK(back.problem.objective == p.objective);
+  CHECK(back.problem.var_bounds.lower == p.var_bounds.lower);
+  CHECK(back.problem.var_bounds.upper == p.var_bounds.upper);
+  CHECK(back.problem.row_bounds.lower == p.row_bounds.lower);
+  CHECK(back.problem.row_bounds.upper == p.row_bounds.upper);
+  CHECK_THROWS_AS(parse_mps_string("ROWS\n L r\nENDATA\n"), MpsParseError);
+}
+
 int main(int argc, char** argv) {
+  if (argc > 6 && std::strcmp(argv[1], "--write-mps") == 0) return write_set_cover_mps(argv + 2);
   if (argc > 2 && std::strcmp(argv[1], "--fsb-c1") == 0) return fsb_c1(argv[2]);
   if (argc > 1 && std::strcmp(argv[1], "--obbt-c2") == 0) return obbt_c2();
   return doctest::shim::run_all(argc, argv);
