@@ -579,6 +579,9 @@ def run_reference(args, world, rank):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
     I.use_generator_library(gen)
+    # all host threads, set before the first reference call: the reference
+    # reads BATCHLP_THREADS once and caches it (sparse.hpp:198-206)
+    cpu_threads()
     root_x = None
     if args.config == "c1":  # root relaxation from the reference solve
         root_x = ref.solve(I.config_problem("c1")).per_problem[0].x

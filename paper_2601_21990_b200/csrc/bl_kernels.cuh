@@ -115,6 +115,28 @@ __device__ __forceinline__ void st_wb(double* p, const double (&v)[V]) {
   }
 }
 
+// Gathered operand rows: read-only path with an L2 eviction-priority hint
+// (BL_GATHER_POLICY 1: evict_last, so the column block being gathered
+// outlives the streamed operands, which are loaded / stored evict-first).
+// The policy lives in the load's memory descriptor (a uniform register).
+#ifndef BL_GATHER_POLICY
+#define BL_GATHER_POLICY 1
+#endif
+template <int V>
+__device__ __forceinline__ void ld_gather(const double* p, double (&o)[V]) {
+  if constexpr (BL_GATHER_POLICY == 0) {
+    ld_nc<V>(p, o);
+  } else {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    if constexpr (V == 2)
+      asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                   : "=d"(o[0]), "=d"(o[1]) : "l"(p), "l"(pol));
+    else
+      asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(o[0]) : "l"(p), "l"(pol));
+  }
+}
+
 // One CSR row of op(A) times the lane's V slots of a column block. The
 // accumulation follows the stored order with separately rounded products
 // and sums: the reference csr_apply (sparse.hpp:176-183) bit for bit.
@@ -160,10 +182,17 @@ __device__ __forceinline__ void gather_row(const int* __restrict__ rp,
     const double a0 = ldd(cv + p), a1 = ldd(cv + p + 1);
     const double a2 = ldd(cv + p + 2), a3 = ldd(cv + p + 3);
     double x0[V], x1[V], x2[V], x3[V];
-    ld_nc<V>(base + (size_t)c0 * W, x0);
-    ld_nc<V>(base + (size_t)c1 * W, x1);
-    ld_nc<V>(base + (size_t)c2 * W, x2);
-    ld_nc<V>(base + (size_t)c3 * W, x3);
+    if constexpr (GENERIC) {
+      ld_nc<V>(base + (size_t)c0 * W, x0);
+      ld_nc<V>(base + (size_t)c1 * W, x1);
+      ld_nc<V>(base + (size_t)c2 * W, x2);
+      ld_nc<V>(base + (size_t)c3 * W, x3);
+    } else {
+      ld_gather<V>(base + (size_t)c0 * W, x0);
+      ld_gather<V>(base + (size_t)c1 * W, x1);
+      ld_gather<V>(base + (size_t)c2 * W, x2);
+      ld_gather<V>(base + (size_t)c3 * W, x3);
+    }
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       acc[v] = __dadd_rn(acc[v], __dmul_rn(a0, x0[v]));
@@ -200,7 +229,7 @@ __device__ __forceinline__ void gather_row(const int* __restrict__ rp,
     for (int k = 0; k < 3; ++k) {
       if (p + k < e) {
         a[k] = ldd(cv + p + k);
-        ld_nc<V>(base + (size_t)ldi(ci + p + k) * W, x[k]);
+        ld_gather<V>(base + (size_t)ldi(ci + p + k) * W, x[k]);
       }
     }
 #pragma unroll
@@ -251,7 +280,7 @@ __device__ __forceinline__ void gather_row_grp(const int* __restrict__ rp,
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        if (t + q < cnt) ld_nc<V>(base + (size_t)c[q] * W, x[q]);
+        if (t + q < cnt) ld_gather<V>(base + (size_t)c[q] * W, x[q]);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         if (t + q < cnt) {
@@ -393,17 +422,21 @@ __device__ __forceinline__ void set_lanes(Op& op, int L) {
 // Walks the work items of a persistent row kernel. Op provides:
 //   begin(b, slot0, acc, owner)  per item (owner: holds the matrix's row 0)
 //   row(b, i, slot0, acc)        per row of the group's contiguous chunk
+#ifndef BL_DYNAMIC_ITEMS
+#define BL_DYNAMIC_ITEMS 1
+#endif
 template <int W, int NS, int LL = 0, class Op>
 __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
                                          double* partials, int* counters,
-                                         double* colsum, int s0, int Kp, double* red) {
+                                         double* colsum, int s0, int Kp, double* red,
+                                         int* ticket = nullptr) {
   using Gm = Geo<W, LL>;
   constexpr int V = Gm::V, L = Gm::L, G = Gm::G;
   SColInfo* s_col = col_smem();
   const int tid = threadIdx.x, g = tid / L, li = tid - g * L;
   const int items = nb * R;
   const int per = R > 0 ? (rows + R - 1) / R : 0;
-  for (int w = blockIdx.x; w < items; w += gridDim.x) {
+  auto item = [&](int w) {
     const int b = w / R, r = w - b * R;
     const int r0 = min(rows, r * per), r1 = min(rows, r0 + per);
     const int cnt = r1 - r0;
@@ -428,8 +461,56 @@ __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
     set_lanes(op, L);
     for (int i = gs; i < ge; ++i) op.row(b, i, slot0, li, acc);
     publish_item<W, NS, LL>(acc, b, r, R, partials, counters, colsum, s0, Kp, red);
+  };
+  if (!BL_DYNAMIC_ITEMS || ticket == nullptr) {
+    for (int w = blockIdx.x; w < items; w += gridDim.x) item(w);
+    return;
+  }
+  // Items handed out in block-major order from one atomic ticket (the next
+  // one fetched while the current item runs): every CTA stays on the column
+  // block the grid is working on, so only ~one block's gathered operand is
+  // live in L2 (a static stride lets slow and fast CTAs drift apart by
+  // blocks). Which CTA runs an item does not change any sum: partials are
+  // indexed by item and folded in item order.
+  __shared__ int s_next[2];
+  if (tid == 0) s_next[0] = atomicAdd(ticket, 1);
+  __syncthreads();
+  int par = 0;
+  for (int w = s_next[0]; w < items; w = s_next[par]) {
+    if (tid == 0) s_next[par ^ 1] = atomicAdd(ticket, 1);
+    item(w);  // ends with a CTA barrier: s_next[par ^ 1] is visible
+    par ^= 1;
+  }
+  // the last CTA to retire re-arms the ticket for the next launch / phase
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(ticket + 1, 1) == (int)gridDim.x - 1) {
+      atomicExch(ticket, 0);
+      atomicExch(ticket + 1, 0);
+      __threadfence();
+    }
   }
 }
+
+// Lanes per row for a pass: full width unless one block is active, then the
+// smallest power of two covering the live slots (narrow tail mapping).
+template <int W>
+__device__ __forceinline__ int pass_lanes(int active) {
+  constexpr int Lfull = Geo<W>::L, V = Geo<W>::V;
+  if (active > W) return Lfull;
+  int L = 1;
+  while (L * V < active && L < Lfull) L <<= 1;
+  return L;
+}
+
+#define BL_DISPATCH_L(W, Lsel, CALL)                                          \
+  switch (Lsel) {                                                            \
+    case 1: if constexpr (Geo<W>::L >= 1) { constexpr int LL_ = 1; CALL; } break;   \
+    case 2: if constexpr (Geo<W>::L >= 2) { constexpr int LL_ = 2; CALL; } break;   \
+    case 4: if constexpr (Geo<W>::L >= 4) { constexpr int LL_ = 4; CALL; } break;   \
+    case 8: if constexpr (Geo<W>::L >= 8) { constexpr int LL_ = 8; CALL; } break;   \
+    default: { constexpr int LL_ = 0; CALL; } break;                         \
+  }
 
 // Effective cost / bounds of one column at one variable (ColumnView,
 // problem.hpp:209-236): base entry or signed unit objective, then the
@@ -588,16 +669,27 @@ static __device__ void primal_body(const Params& P, const Ctrl& C, double* red) 
   prof_begin(P, K_PRIMAL);
   PrimalOp<W, CHECK> op(P, C);
   const int nb = (C.active + W - 1) / W;
-  run_rows<W, 2, LL>(op, P.n, nb, C.Rp, P.partials, P.counters, P.colsum, S_DX2, P.Kp, red);
+  run_rows<W, 2, LL>(op, P.n, nb, C.Rp, P.partials, P.counters, P.colsum, S_DX2, P.Kp, red,
+                     P.ticket);
   prof_end(P, K_PRIMAL);
 }
 
+// BL_NARROW_ROWS: with one column block left the graph's row kernels walk
+// rows with the narrow lane mapping (only the live slots are gathered).
+#ifndef BL_NARROW_ROWS
+#define BL_NARROW_ROWS 1
+#endif
 template <int W, bool CHECK>
 __global__ void __launch_bounds__(kBlock, kPrimalMinCtas) k_primal(Params P) {
   __shared__ double red[kRedDoubles];
   const Ctrl C = *P.ctrl;
   if (C.done) return;
-  primal_body<W, CHECK>(P, C, red);
+  if constexpr (BL_NARROW_ROWS && W >= 16) {
+    const int Lsel = pass_lanes<W>(C.active);
+    BL_DISPATCH_L(W, Lsel, (primal_body<W, CHECK, LL_>(P, C, red)));
+  } else {
+    primal_body<W, CHECK>(P, C, red);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -709,7 +801,7 @@ static __device__ void dual_body(const Params& P, const Ctrl& C, double* red) {
   DualOp<W, CHECK, GRP> op(P, C);
   const int nb = (C.active + W - 1) / W;
   run_rows<W, DualOp<W, CHECK, GRP>::NS, LL>(op, P.m, nb, C.Rd, P.partials, P.counters,
-                                    P.colsum, S_DY2, P.Kp, red);
+                                    P.colsum, S_DY2, P.Kp, red, P.ticket);
   prof_end(P, K_DUAL);
 }
 
@@ -718,7 +810,12 @@ __global__ void __launch_bounds__(kBlock, kDualMinCtas) k_dual(Params P) {
   __shared__ double red[kRedDoubles];
   const Ctrl C = *P.ctrl;
   if (C.done) return;
-  dual_body<W, CHECK>(P, C, red);
+  if constexpr (BL_NARROW_ROWS && W >= 16) {
+    const int Lsel = pass_lanes<W>(C.active);
+    BL_DISPATCH_L(W, Lsel, (dual_body<W, CHECK, LL_>(P, C, red)));
+  } else {
+    dual_body<W, CHECK>(P, C, red);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -804,7 +901,8 @@ static __device__ void check_body(const Params& P, const Ctrl& C, double* red) {
   prof_begin(P, K_CHECK);
   CheckOp<W> op(P, C);
   const int nb = (C.active + W - 1) / W;
-  run_rows<W, 10, LL>(op, P.n, nb, C.Rc, P.partials, P.counters, P.colsum, S_OBJ, P.Kp, red);
+  run_rows<W, 10, LL>(op, P.n, nb, C.Rc, P.partials, P.counters, P.colsum, S_OBJ, P.Kp, red,
+                      P.ticket);
   prof_end(P, K_CHECK);
 }
 
@@ -813,7 +911,12 @@ __global__ void __launch_bounds__(kBlock, kRowMinCtas) k_check(Params P) {
   __shared__ double red[kRedDoubles];
   const Ctrl C = *P.ctrl;
   if (C.done || !C.check) return;
-  check_body<W>(P, C, red);
+  if constexpr (BL_NARROW_ROWS && W >= 16) {
+    const int Lsel = pass_lanes<W>(C.active);
+    BL_DISPATCH_L(W, Lsel, (check_body<W, LL_>(P, C, red)));
+  } else {
+    check_body<W>(P, C, red);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -855,7 +958,8 @@ static __device__ void cert_body(const Params& P, const Ctrl& C, double* red) {
   prof_begin(P, K_CERT);
   CertOp<W> op(P, C);
   const int nb = (C.active + W - 1) / W;
-  run_rows<W, 1, LL>(op, P.n, nb, C.Rc, P.partials, P.counters, P.colsum, S_CERT, P.Kp, red);
+  run_rows<W, 1, LL>(op, P.n, nb, C.Rc, P.partials, P.counters, P.colsum, S_CERT, P.Kp, red,
+                     P.ticket);
   prof_end(P, K_CERT);
 }
 
@@ -1779,26 +1883,6 @@ __device__ __forceinline__ void loop_rows(const Params& P, const Ctrl& C, double
     sync();
   }
 }
-
-// Lanes per row for a pass: full width unless one block is active, then the
-// smallest power of two covering the live slots (narrow tail mapping).
-template <int W>
-__device__ __forceinline__ int pass_lanes(int active) {
-  constexpr int Lfull = Geo<W>::L, V = Geo<W>::V;
-  if (active > W) return Lfull;
-  int L = 1;
-  while (L * V < active && L < Lfull) L <<= 1;
-  return L;
-}
-
-#define BL_DISPATCH_L(W, Lsel, CALL)                                          \
-  switch (Lsel) {                                                            \
-    case 1: if constexpr (Geo<W>::L >= 1) { constexpr int LL_ = 1; CALL; } break;   \
-    case 2: if constexpr (Geo<W>::L >= 2) { constexpr int LL_ = 2; CALL; } break;   \
-    case 4: if constexpr (Geo<W>::L >= 4) { constexpr int LL_ = 4; CALL; } break;   \
-    case 8: if constexpr (Geo<W>::L >= 8) { constexpr int LL_ = 8; CALL; } break;   \
-    default: { constexpr int LL_ = 0; CALL; } break;                         \
-  }
 
 // ---------------------------------------------------------------------------
 // fast tail passes: one cluster, one active column block, plain iteration

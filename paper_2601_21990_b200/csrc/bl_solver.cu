@@ -792,7 +792,10 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
                                                        items_for(n, W, grid)));
   P.partials = static_cast<double*>(
       ctx->buf[bl_ctx::B_PART].ensure(sizeof(double) * max_items * 10 * W));
-  P.counters = static_cast<int*>(ctx->buf[bl_ctx::B_CNT].ensure(sizeof(int) * (size_t)std::max(nb, 64)));
+  // per-block fold counters, then the row kernels' work-item ticket
+  P.counters = static_cast<int*>(
+      ctx->buf[bl_ctx::B_CNT].ensure(sizeof(int) * ((size_t)std::max(nb, 64) + 2)));
+  P.ticket = P.counters + std::max(nb, 64);
   P.snap_list = static_cast<int*>(ctx->buf[bl_ctx::B_SNAP].ensure(sizeof(int) * 3 * (size_t)Kp));
   P.moves = static_cast<int*>(ctx->buf[bl_ctx::B_MOVES].ensure(sizeof(int) * 2 * (size_t)Kp));
   P.log_cap = 1 << 16;
@@ -919,7 +922,7 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
       hoi[2 * (size_t)width + j] = oe[j];
     }
     ck(cudaMemcpyAsync(oi, hoi.data(), sizeof(int) * hoi.size(), cudaMemcpyHostToDevice, s), "origi");
-    ck(cudaMemsetAsync(P.counters, 0, sizeof(int) * (size_t)std::max(nb, 64), s), "counters");
+    ck(cudaMemsetAsync(P.counters, 0, sizeof(int) * ((size_t)std::max(nb, 64) + 2), s), "counters");
     ck(cudaMemsetAsync(P.res, 0, sizeof(bl_column_result) * (size_t)width, s), "res");
     ck(cudaMemsetAsync(P.colsum, 0, sizeof(double) * bl::S_COUNT * (size_t)Kp, s), "colsum");
   }
