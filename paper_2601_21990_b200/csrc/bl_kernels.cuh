@@ -137,6 +137,54 @@ __device__ __forceinline__ void ld_gather(const double* p, double (&o)[V]) {
   }
 }
 
+// ---- cp.async staging of the streamed operands ----------------------------
+// Each lane copies its own V doubles of a row's streamed operands (X, aX in
+// the primal; Y, AX, aY, aAX in the dual) into shared memory one row ahead,
+// so their latency overlaps the current row's gathers without holding
+// registers: the registers go to deeper gather batches instead. A lane only
+// reads back what it copied itself, so cp.async.wait_group is the only sync.
+#ifndef BL_STAGE
+#define BL_STAGE 1
+#endif
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <int V>
+__device__ __forceinline__ void cp_stream(double* dst, const double* src) {
+  const unsigned long long pol = policy_evict_first();
+  if constexpr (V == 2)
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
+                 :: "r"(smem_addr(dst)), "l"(src), "l"(pol) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;"
+                 :: "r"(smem_addr(dst)), "l"(src), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory");
+}
+template <int V>
+__device__ __forceinline__ void ld_stage(const double* p, double (&o)[V]) {
+  if constexpr (V == 2) {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    o[0] = t.x;
+    o[1] = t.y;
+  } else {
+    o[0] = *p;
+  }
+}
+// lane tid's copy of streamed operand k in stage st
+template <int V, int NOPS>
+__device__ __forceinline__ double* stage_slot(double* stg, int st, int k) {
+  return stg + ((size_t)(st * NOPS + k) * kBlock + threadIdx.x) * V;
+}
+
 // One CSR row of op(A) times the lane's V slots of a column block. The
 // accumulation follows the stored order with separately rounded products
 // and sums: the reference csr_apply (sparse.hpp:176-183) bit for bit.
@@ -291,6 +339,55 @@ __device__ __forceinline__ void gather_row_grp(const int* __restrict__ rp,
   }
 }
 
+// The cooperative product with D gathers in flight per batch (D = 8 when
+// the streamed operands are staged in shared memory and the registers are
+// free): one metadata round trip per L nonzeros, ceil(cnt / D) gather round
+// trips. Same summation order.
+#ifndef BL_GATHER_DEPTH
+#define BL_GATHER_DEPTH 8
+#endif
+template <int W, int D>
+__device__ __forceinline__ void gather_row_deep(const int* __restrict__ rp,
+                                                const int* __restrict__ ci,
+                                                const double* __restrict__ cv,
+                                                const double* __restrict__ base, int i, int L,
+                                                double (&acc)[Geo<W>::V]) {
+  constexpr int V = Geo<W>::V;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (L - 1);
+  const unsigned mask = L >= 32 ? 0xffffffffu : (((1u << L) - 1u) << (lane & ~(L - 1)));
+  const int p = __ldg(rp + i);
+  const int e = __ldg(rp + i + 1);
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.0;
+  for (int ch = p; ch < e; ch += L) {
+    const int k = ch + gl;
+    int myc = 0;
+    double myv = 0.0;
+    if (k < e) {
+      myc = __ldg(ci + k);
+      myv = __ldg(cv + k);
+    }
+    const int cnt = min(L, e - ch);
+    for (int t = 0; t < cnt; t += D) {
+      double x[D][V];
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        const int c = __shfl_sync(mask, myc, t + q, L);
+        if (t + q < cnt) ld_gather<V>(base + (size_t)c * W, x[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        const double a = __shfl_sync(mask, myv, t + q, L);
+        if (t + q < cnt) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[v] = __dadd_rn(acc[v], __dmul_rn(a, x[q][v]));
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // deterministic per-column reduction of one work item
 // ---------------------------------------------------------------------------
@@ -382,6 +479,7 @@ __device__ __forceinline__ void publish_item(double (&acc)[NS][Geo<W>::V], int b
 struct SColInfo {
   int valid, orig, ob, oe, v0, k0;
   double val0, step;
+  int fast, pad;  // fast: single-point column (see ColInfo)
 };
 
 // One shared array of column descriptors per CTA, whichever run_rows
@@ -425,7 +523,7 @@ __device__ __forceinline__ void set_lanes(Op& op, int L) {
 #ifndef BL_DYNAMIC_ITEMS
 #define BL_DYNAMIC_ITEMS 1
 #endif
-template <int W, int NS, int LL = 0, class Op>
+template <int W, int NS, int LL = 0, bool STG = false, class Op>
 __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
                                          double* partials, int* counters,
                                          double* colsum, int s0, int Kp, double* red,
@@ -459,7 +557,22 @@ __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
     __syncthreads();
     op.begin(b, slot0, acc, r == 0 && g == 0, &s_col[li * V]);
     set_lanes(op, L);
-    for (int i = gs; i < ge; ++i) op.row(b, i, slot0, li, acc);
+    if constexpr (STG && BL_STAGE && Op::kStreams > 0) {
+      // row i's streamed operands were copied while row i - 1 ran
+      if (gs < ge) op.prefetch(b, gs, li, red, 0);
+      cp_commit();
+      for (int i = gs; i < ge; ++i) {
+        const int st = (i - gs) & 1;
+        if (i + 1 < ge) op.prefetch(b, i + 1, li, red, st ^ 1);
+        cp_commit();
+        cp_wait<1>();
+        op.row_staged(b, i, li, acc, red, st);
+      }
+      cp_wait<0>();
+      __syncthreads();  // the staging ring is the reduction scratch
+    } else {
+      for (int i = gs; i < ge; ++i) op.row(b, i, slot0, li, acc);
+    }
     publish_item<W, NS, LL>(acc, b, r, R, partials, counters, colsum, s0, Kp, red);
   };
   if (!BL_DYNAMIC_ITEMS || ticket == nullptr) {
@@ -515,9 +628,15 @@ __device__ __forceinline__ int pass_lanes(int active) {
 // Effective cost / bounds of one column at one variable (ColumnView,
 // problem.hpp:209-236): base entry or signed unit objective, then the
 // column's overrides in list order (later entries win).
+// fast: the column equals the base row data (zero cost in signed-unit mode)
+// except at most at one variable v0 where (k0, val0) applies -- every FSB
+// column (<= 1 bound override) and every OBBT column (its signed unit,
+// canonicalised into v0 = the unit's variable, an objective entry of +-1).
+// Other columns walk the general rule.
 struct ColInfo {
   int valid, orig, ob, oe, v0, k0;
   double val0, step;
+  int fast;
 };
 
 __device__ __forceinline__ void load_col(const Params& P, int j, int active,
@@ -533,6 +652,17 @@ __device__ __forceinline__ void load_col(const Params& P, int j, int active,
     c.v0 = P.ov_var[c.ob];
     c.k0 = P.ov_kind[c.ob];
     c.val0 = P.ov_val[c.ob];
+  }
+  if (P.mode == BL_SIGNED_UNIT_COLUMNS) {
+    c.fast = c.oe == c.ob;
+    if (c.fast) {  // the unit itself is the single point
+      const int o = c.orig + P.unit_off, n = P.n;
+      c.v0 = o < n ? o : o - n;
+      c.k0 = BL_OVERRIDE_OBJECTIVE;
+      c.val0 = o < n ? 1.0 : -1.0;
+    }
+  } else {
+    c.fast = c.oe - c.ob <= 1;
   }
   // StepParams (solver.hpp:58-59): tau = eta / w, sigma = eta * w
   const double w = c.valid ? P.w[j] : 1.0;
@@ -552,6 +682,10 @@ __device__ __forceinline__ void col_vals(const Params& P, const ColInfo& c, int 
   cc = bc;
   lo = bl;
   hi = bh;
+  if (c.fast) {
+    if (c.v0 == i) apply_ov(c.k0, c.val0, cc, lo, hi);
+    return;
+  }
   if (P.mode == BL_SIGNED_UNIT_COLUMNS) {
     const int n = P.n, o = c.orig + P.unit_off;
     cc = o < n ? (i == o ? 1.0 : 0.0) : (i == o - n ? -1.0 : 0.0);
@@ -575,6 +709,7 @@ __device__ __forceinline__ ColInfo read_col(const volatile SColInfo* s) {
   c.k0 = s->k0;
   c.val0 = s->val0;
   c.step = s->step;
+  c.fast = s->fast;
   return c;
 }
 __device__ __forceinline__ void stage_col(const Params& P, int j, int active, bool dual_step,
@@ -589,13 +724,14 @@ __device__ __forceinline__ void stage_col(const Params& P, int j, int active, bo
   s->k0 = c.k0;
   s->val0 = c.val0;
   s->step = c.step;
+  s->fast = c.fast;
 }
 
 // ---------------------------------------------------------------------------
 // primal: XT = proj(X - tau (c + A'Y)), X' = Halpern, sums
 // ---------------------------------------------------------------------------
 // GEN: the CSR arrays may be the tail's shared-memory cache (generic loads)
-template <int W, bool CHECK, bool GEN = false>
+template <int W, bool CHECK, bool GEN = false, bool LAZY = false>
 struct PrimalOp {
   static constexpr int V = Geo<W>::V;
   const Params& P;
@@ -608,7 +744,40 @@ struct PrimalOp {
   const int* cci;
   const double* ccv;
   int lanes = Geo<W>::L;  // lanes per row group (narrow tail mappings use fewer)
+  // LAZY (the staged graph kernels): the control block lives in the CTA's
+  // shared memory and every per-launch scalar / pointer is re-read from it
+  // or from the kernel parameters where it is used, so none of them pins
+  // a register across the gather loop.
+  const Ctrl* lc = nullptr;
+  __device__ __forceinline__ int reset_() const {
+    if constexpr (LAZY) return lc->anchor_reset; else return reset;
+  }
+  __device__ __forceinline__ double alpha_() const {
+    if constexpr (LAZY) return lc->alpha; else return alpha;
+  }
+  __device__ __forceinline__ double oma_() const {
+    if constexpr (LAZY) return 1.0 - lc->alpha; else return oma;
+  }
+  __device__ __forceinline__ const double* Ycur_() const {
+    if constexpr (LAZY) return P.Y[lc->cur]; else return Ycur;
+  }
+  __device__ __forceinline__ const double* Xcur_() const {
+    if constexpr (LAZY) return P.X[lc->cur]; else return Xcur;
+  }
+  __device__ __forceinline__ double* Xnxt_() const {
+    if constexpr (LAZY) return P.X[lc->cur ^ 1]; else return Xnxt;
+  }
+  __device__ __forceinline__ const int* crp_() const {
+    if constexpr (LAZY) return P.trp; else return crp;
+  }
+  __device__ __forceinline__ const int* cci_() const {
+    if constexpr (LAZY) return P.tci; else return cci;
+  }
+  __device__ __forceinline__ const double* ccv_() const {
+    if constexpr (LAZY) return P.tcv; else return ccv;
+  }
   __device__ PrimalOp(const Params& p, const Ctrl& C) : P(p) {
+    if constexpr (LAZY) lc = &C;
     crp = P.trp;
     cci = P.tci;
     ccv = P.tcv;
@@ -624,15 +793,74 @@ struct PrimalOp {
   __device__ void begin(int, int, double (&)[2][V], bool, const volatile SColInfo* sc) {
     col = sc;
   }
+  // streamed operands staged through shared memory (not for the tail's
+  // cached-metadata rows, which run their own schedule)
+  static constexpr int kStreams = GEN ? 0 : 2;
+  __device__ void prefetch(int b, int i, int li, double* stg, int st) {
+    const size_t idx = ((size_t)b * P.n + i) * W + li * V;
+    cp_stream<V>(stage_slot<V, 2>(stg, st, 0), Xcur_() + idx);
+    if (!reset_()) cp_stream<V>(stage_slot<V, 2>(stg, st, 1), P.aX + idx);
+  }
+  __device__ void row_staged(int b, int i, int li, double (&acc)[2][V], const double* stg,
+                             int st) {
+    const int n = P.n, m = P.m;
+    const double bc = P.mode == BL_SHARED_OBJECTIVE ? __ldg(P.c + i) : 0.0;
+    const double bl = __ldg(P.xl + i), bh = __ldg(P.xu + i);
+    const size_t idx = ((size_t)b * n + i) * W + li * V;
+    double aty[V];
+    if (lanes >= 8)
+      gather_row_deep<W, BL_GATHER_DEPTH>(crp_(), cci_(), ccv_(), Ycur_() + (size_t)b * m * W + li * V, i, lanes, aty);
+    else
+      gather_row<W>(crp_(), cci_(), ccv_(), Ycur_() + (size_t)b * m * W + li * V, i, aty);
+    double x[V], ax[V];
+    ld_stage<V>(stage_slot<V, 2>(const_cast<double*>(stg), st, 0), x);
+    if (reset_()) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) ax[v] = x[v];
+    } else {
+      ld_stage<V>(stage_slot<V, 2>(const_cast<double*>(stg), st, 1), ax);
+    }
+    finish(idx, i, bc, bl, bh, x, ax, aty, acc);
+  }
+  __device__ __forceinline__ void finish(size_t idx, int i, double bc, double bl, double bh,
+                                         const double (&x)[V], const double (&ax)[V],
+                                         const double (&aty)[V], double (&acc)[2][V]) {
+    double xt[V], xn[V], rc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      // descriptor fields read where needed (volatile: not kept in registers)
+      const volatile SColInfo* sc = col + v;
+      double cc = bc, lo = bl, hi = bh;
+      if (sc->fast) {
+        if (sc->v0 == i) apply_ov(sc->k0, sc->val0, cc, lo, hi);
+      } else {
+        col_vals(P, read_col(sc), i, bc, bl, bh, cc, lo, hi);
+      }
+      const double t = cc + aty[v];
+      xt[v] = project_box(x[v] - sc->step * t, lo, hi);
+      const double dx = xt[v] - x[v];
+      const double da = x[v] - ax[v];
+      if (sc->valid) {
+        acc[0][v] += dx * dx;
+        acc[1][v] += da * da;
+      }
+      xn[v] = alpha_() * (2.0 * xt[v] - x[v]) + oma_() * ax[v];
+      if (CHECK) rc[v] = project_barrier(-cc - aty[v], lo, hi);
+    }
+    st_wb<V>(P.XT + idx, xt);
+    st_cs<V>(Xnxt_() + idx, xn);
+    if (reset_()) st_cs<V>(P.aX + idx, x);
+    if (CHECK) st_wb<V>(P.RC + idx, rc);
+  }
   __device__ void row(int b, int i, int, int li, double (&acc)[2][V]) {
     const int n = P.n, m = P.m;
     // streamed operands first, so their latency overlaps the gathers
     const double bc = P.mode == BL_SHARED_OBJECTIVE ? __ldg(P.c + i) : 0.0;
     const double bl = __ldg(P.xl + i), bh = __ldg(P.xu + i);
     const size_t idx = ((size_t)b * n + i) * W + li * V;
-    double x[V], ax[V], xt[V], xn[V], rc[V];
-    ld_cs<V>(Xcur + idx, x);
-    if (reset) {
+    double x[V], ax[V];
+    ld_cs<V>(Xcur_() + idx, x);
+    if (reset_()) {
 #pragma unroll
       for (int v = 0; v < V; ++v) ax[v] = x[v];
     } else {
@@ -640,36 +868,20 @@ struct PrimalOp {
     }
     double aty[V];
     // (the cooperative-metadata gather measured slower for A' rows: short rows)
-    gather_row<W, GEN>(crp, cci, ccv, Ycur + (size_t)b * m * W + li * V, i, aty);
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const ColInfo cl = read_col(col + v);
-      double cc, lo, hi;
-      col_vals(P, cl, i, bc, bl, bh, cc, lo, hi);
-      const double t = cc + aty[v];
-      xt[v] = project_box(x[v] - cl.step * t, lo, hi);
-      const double dx = xt[v] - x[v];
-      const double da = x[v] - ax[v];
-      if (cl.valid) {
-        acc[0][v] += dx * dx;
-        acc[1][v] += da * da;
-      }
-      xn[v] = alpha * (2.0 * xt[v] - x[v]) + oma * ax[v];
-      if (CHECK) rc[v] = project_barrier(-cc - aty[v], lo, hi);
-    }
-    st_wb<V>(P.XT + idx, xt);
-    st_cs<V>(Xnxt + idx, xn);
-    if (reset) st_cs<V>(P.aX + idx, x);
-    if (CHECK) st_wb<V>(P.RC + idx, rc);
+    gather_row<W, GEN>(crp_(), cci_(), ccv_(), Ycur_() + (size_t)b * m * W + li * V, i, aty);
+    finish(idx, i, bc, bl, bh, x, ax, aty, acc);
   }
 };
 
-template <int W, bool CHECK, int LL = 0>
+// STG: stage the streamed operands through `red` (kRowSmemDoubles; the
+// graph's row kernels). The persistent / cluster loop kernels keep the
+// register path (their static shared memory has no room for the ring).
+template <int W, bool CHECK, int LL = 0, bool STG = false>
 static __device__ void primal_body(const Params& P, const Ctrl& C, double* red) {
   prof_begin(P, K_PRIMAL);
-  PrimalOp<W, CHECK> op(P, C);
+  PrimalOp<W, CHECK, false, STG> op(P, C);  // STG: C is in shared memory
   const int nb = (C.active + W - 1) / W;
-  run_rows<W, 2, LL>(op, P.n, nb, C.Rp, P.partials, P.counters, P.colsum, S_DX2, P.Kp, red,
+  run_rows<W, 2, LL, STG>(op, P.n, nb, C.Rp, P.partials, P.counters, P.colsum, S_DX2, P.Kp, red,
                      P.ticket);
   prof_end(P, K_PRIMAL);
 }
@@ -681,21 +893,23 @@ static __device__ void primal_body(const Params& P, const Ctrl& C, double* red) 
 #endif
 template <int W, bool CHECK>
 __global__ void __launch_bounds__(kBlock, kPrimalMinCtas) k_primal(Params P) {
-  __shared__ double red[kRedDoubles];
-  const Ctrl C = *P.ctrl;
+  __shared__ __align__(16) double red[kRowSmemDoubles];
+  __shared__ Ctrl C;  // shared: the staged row ops re-read it per row
+  if (threadIdx.x == 0) C = *P.ctrl;
+  __syncthreads();
   if (C.done) return;
   if constexpr (BL_NARROW_ROWS && W >= 16) {
     const int Lsel = pass_lanes<W>(C.active);
-    BL_DISPATCH_L(W, Lsel, (primal_body<W, CHECK, LL_>(P, C, red)));
+    BL_DISPATCH_L(W, Lsel, (primal_body<W, CHECK, LL_, true>(P, C, red)));
   } else {
-    primal_body<W, CHECK>(P, C, red);
+    primal_body<W, CHECK, 0, true>(P, C, red);
   }
 }
 
 // ---------------------------------------------------------------------------
 // dual: AXT = A XT, YT = sigma (s - proj(s)), Y'/AX' = Halpern, sums
 // ---------------------------------------------------------------------------
-template <int W, bool CHECK, bool GRP = true, bool GEN = false>
+template <int W, bool CHECK, bool GRP = true, bool GEN = false, bool LAZY = false>
 struct DualOp {
   static constexpr int V = Geo<W>::V;
   static constexpr int NS = CHECK ? 9 : 3;
@@ -709,7 +923,43 @@ struct DualOp {
   const int* cci;
   const double* ccv;
   int lanes = Geo<W>::L;
+  // LAZY (the staged graph kernels): the control block lives in the CTA's
+  // shared memory and every per-launch scalar / pointer is re-read from it
+  // or from the kernel parameters where it is used, so none of them pins
+  // a register across the gather loop.
+  const Ctrl* lc = nullptr;
+  __device__ __forceinline__ int reset_() const {
+    if constexpr (LAZY) return lc->anchor_reset; else return reset;
+  }
+  __device__ __forceinline__ double alpha_() const {
+    if constexpr (LAZY) return lc->alpha; else return alpha;
+  }
+  __device__ __forceinline__ double oma_() const {
+    if constexpr (LAZY) return 1.0 - lc->alpha; else return oma;
+  }
+  __device__ __forceinline__ const double* Ycur_() const {
+    if constexpr (LAZY) return P.Y[lc->cur]; else return Ycur;
+  }
+  __device__ __forceinline__ const double* AXcur_() const {
+    if constexpr (LAZY) return P.AX[lc->cur]; else return AXcur;
+  }
+  __device__ __forceinline__ double* Ynxt_() const {
+    if constexpr (LAZY) return P.Y[lc->cur ^ 1]; else return Ynxt;
+  }
+  __device__ __forceinline__ double* AXnxt_() const {
+    if constexpr (LAZY) return P.AX[lc->cur ^ 1]; else return AXnxt;
+  }
+  __device__ __forceinline__ const int* crp_() const {
+    if constexpr (LAZY) return P.rp; else return crp;
+  }
+  __device__ __forceinline__ const int* cci_() const {
+    if constexpr (LAZY) return P.ci; else return cci;
+  }
+  __device__ __forceinline__ const double* ccv_() const {
+    if constexpr (LAZY) return P.cv; else return ccv;
+  }
   __device__ DualOp(const Params& p, const Ctrl& C) : P(p) {
+    if constexpr (LAZY) lc = &C;
     crp = P.rp;
     cci = P.ci;
     ccv = P.cv;
@@ -726,14 +976,50 @@ struct DualOp {
   __device__ void begin(int, int, double (&)[NS][V], bool, const volatile SColInfo* sc) {
     col = sc;
   }
+  static constexpr int kStreams = GEN ? 0 : 4;
+  __device__ void prefetch(int b, int i, int li, double* stg, int st) {
+    const size_t idx = ((size_t)b * P.m + i) * W + li * V;
+    cp_stream<V>(stage_slot<V, 4>(stg, st, 0), Ycur_() + idx);
+    cp_stream<V>(stage_slot<V, 4>(stg, st, 1), AXcur_() + idx);
+    if (!reset_()) {
+      cp_stream<V>(stage_slot<V, 4>(stg, st, 2), P.aY + idx);
+      cp_stream<V>(stage_slot<V, 4>(stg, st, 3), P.aAX + idx);
+    }
+  }
+  __device__ void row_staged(int b, int i, int li, double (&acc)[NS][V], const double* stg,
+                             int st) {
+    const int n = P.n, m = P.m;
+    const double lo = __ldg(P.rl + i), hi = __ldg(P.ru + i);
+    const size_t idx = ((size_t)b * m + i) * W + li * V;
+    double axt[V];
+    if (lanes >= 8)
+      gather_row_deep<W, BL_GATHER_DEPTH>(crp_(), cci_(), ccv_(), P.XT + (size_t)b * n * W + li * V, i, lanes, axt);
+    else
+      gather_row<W>(crp_(), cci_(), ccv_(), P.XT + (size_t)b * n * W + li * V, i, axt);
+    double* sg = const_cast<double*>(stg);
+    double y[V], ax[V], ay[V], aax[V];
+    ld_stage<V>(stage_slot<V, 4>(sg, st, 0), y);
+    ld_stage<V>(stage_slot<V, 4>(sg, st, 1), ax);
+    if (reset_()) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        ay[v] = y[v];
+        aax[v] = ax[v];
+      }
+    } else {
+      ld_stage<V>(stage_slot<V, 4>(sg, st, 2), ay);
+      ld_stage<V>(stage_slot<V, 4>(sg, st, 3), aax);
+    }
+    finish(idx, lo, hi, y, ax, ay, aax, axt, acc);
+  }
   __device__ void row(int b, int i, int, int li, double (&acc)[NS][V]) {
     const int n = P.n, m = P.m;
     const double lo = __ldg(P.rl + i), hi = __ldg(P.ru + i);
     const size_t idx = ((size_t)b * m + i) * W + li * V;
-    double y[V], ax[V], ay[V], aax[V], yt[V], yn[V], axn[V], dyb[V];
-    ld_cs<V>(Ycur + idx, y);
-    ld_cs<V>(AXcur + idx, ax);
-    if (reset) {
+    double y[V], ax[V], ay[V], aax[V];
+    ld_cs<V>(Ycur_() + idx, y);
+    ld_cs<V>(AXcur_() + idx, ax);
+    if (reset_()) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         ay[v] = y[v];
@@ -744,30 +1030,38 @@ struct DualOp {
       ld_cs<V>(P.aAX + idx, aax);
     }
     double axt[V];
-    if (GEN) gather_row<W, true>(crp, cci, ccv, P.XT + (size_t)b * n * W + li * V, i, axt);
+    if (GEN) gather_row<W, true>(crp_(), cci_(), ccv_(), P.XT + (size_t)b * n * W + li * V, i, axt);
     else if (GRP && lanes >= 4)
-      gather_row_grp<W>(crp, cci, ccv, P.XT + (size_t)b * n * W + li * V, i, lanes, axt);
-    else gather_row<W>(crp, cci, ccv, P.XT + (size_t)b * n * W + li * V, i, axt);
+      gather_row_grp<W>(crp_(), cci_(), ccv_(), P.XT + (size_t)b * n * W + li * V, i, lanes, axt);
+    else gather_row<W>(crp_(), cci_(), ccv_(), P.XT + (size_t)b * n * W + li * V, i, axt);
+    finish(idx, lo, hi, y, ax, ay, aax, axt, acc);
+  }
+  __device__ __forceinline__ void finish(size_t idx, double lo, double hi, const double (&y)[V],
+                                         const double (&ax)[V], const double (&ay)[V],
+                                         const double (&aax)[V], const double (&axt)[V],
+                                         double (&acc)[NS][V]) {
+    double yt[V], yn[V], axn[V], dyb[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const ColInfo cl = read_col(col + v);
-      const double sigma = cl.step;
+      const volatile SColInfo* sc = col + v;
+      const double sigma = sc->step;
+      const int valid = sc->valid;
       // dual_step_element, solver.hpp:186-190
       const double vv = 2.0 * axt[v] - ax[v];
       const double s = y[v] / sigma + vv;
       yt[v] = sigma * (s - project_box(s, lo, hi));
       const double dy = yt[v] - y[v];
       const double da = y[v] - ay[v];
-      if (cl.valid) {
+      if (valid) {
         acc[0][v] += dy * dy;
         acc[1][v] += dy * (axt[v] - ax[v]);
         acc[2][v] += da * da;
       }
-      yn[v] = alpha * (2.0 * yt[v] - y[v]) + oma * ay[v];
-      axn[v] = alpha * (2.0 * axt[v] - ax[v]) + oma * aax[v];
+      yn[v] = alpha_() * (2.0 * yt[v] - y[v]) + oma_() * ay[v];
+      axn[v] = alpha_() * (2.0 * axt[v] - ax[v]) + oma_() * aax[v];
       if constexpr (CHECK) {
         dyb[v] = project_barrier(yt[v] - y[v], lo, hi);
-        if (cl.valid) {
+        if (valid) {
           acc[3][v] += support_term(yt[v], lo, hi);
           const double viol = axt[v] - project_box(axt[v], lo, hi);
           acc[4][v] += viol * viol;
@@ -781,9 +1075,9 @@ struct DualOp {
         }
       }
     }
-    st_cs<V>(Ynxt + idx, yn);
-    st_cs<V>(AXnxt + idx, axn);
-    if (reset) {
+    st_cs<V>(Ynxt_() + idx, yn);
+    st_cs<V>(AXnxt_() + idx, axn);
+    if (reset_()) {
       st_cs<V>(P.aY + idx, y);
       st_cs<V>(P.aAX + idx, ax);
     }
@@ -795,26 +1089,28 @@ struct DualOp {
   }
 };
 
-template <int W, bool CHECK, int LL = 0, bool GRP = true>
+template <int W, bool CHECK, int LL = 0, bool GRP = true, bool STG = false>
 static __device__ void dual_body(const Params& P, const Ctrl& C, double* red) {
   prof_begin(P, K_DUAL);
-  DualOp<W, CHECK, GRP> op(P, C);
+  DualOp<W, CHECK, GRP, false, STG> op(P, C);  // STG: C is in shared memory
   const int nb = (C.active + W - 1) / W;
-  run_rows<W, DualOp<W, CHECK, GRP>::NS, LL>(op, P.m, nb, C.Rd, P.partials, P.counters,
+  run_rows<W, DualOp<W, CHECK, GRP, false, STG>::NS, LL, STG>(op, P.m, nb, C.Rd, P.partials, P.counters,
                                     P.colsum, S_DY2, P.Kp, red, P.ticket);
   prof_end(P, K_DUAL);
 }
 
 template <int W, bool CHECK>
 __global__ void __launch_bounds__(kBlock, kDualMinCtas) k_dual(Params P) {
-  __shared__ double red[kRedDoubles];
-  const Ctrl C = *P.ctrl;
+  __shared__ __align__(16) double red[kRowSmemDoubles];
+  __shared__ Ctrl C;  // shared: the staged row ops re-read it per row
+  if (threadIdx.x == 0) C = *P.ctrl;
+  __syncthreads();
   if (C.done) return;
   if constexpr (BL_NARROW_ROWS && W >= 16) {
     const int Lsel = pass_lanes<W>(C.active);
-    BL_DISPATCH_L(W, Lsel, (dual_body<W, CHECK, LL_>(P, C, red)));
+    BL_DISPATCH_L(W, Lsel, (dual_body<W, CHECK, LL_, true, true>(P, C, red)));
   } else {
-    dual_body<W, CHECK>(P, C, red);
+    dual_body<W, CHECK, 0, true, true>(P, C, red);
   }
 }
 
@@ -824,6 +1120,7 @@ __global__ void __launch_bounds__(kBlock, kDualMinCtas) k_dual(Params P) {
 template <int W>
 struct CheckOp {
   static constexpr int V = Geo<W>::V;
+  static constexpr int kStreams = 0;
   static constexpr int NS = 10;
   const Params& P;
   int active;
@@ -925,6 +1222,7 @@ __global__ void __launch_bounds__(kBlock, kRowMinCtas) k_check(Params P) {
 template <int W>
 struct CertOp {
   static constexpr int V = Geo<W>::V;
+  static constexpr int kStreams = 0;
   const Params& P;
   int active;
   int flag[V];
@@ -977,6 +1275,7 @@ __global__ void __launch_bounds__(kBlock, kRowMinCtas) k_cert(Params P) {
 template <int W>
 struct SpmmOp {
   static constexpr int V = Geo<W>::V;
+  static constexpr int kStreams = 0;
   const int *rp, *ci;
   const double *cv, *in;
   double* out;
@@ -1198,6 +1497,18 @@ __device__ __forceinline__ void set_cond(const Params& P,
                                          cudaGraphConditionalHandle h,
                                          unsigned v) {
   if (P.use_graph) cudaGraphSetConditional(h, v);
+}
+// Handle values persist through the WHILE loop of one graph launch (they
+// are reset to their defaults only when the graph is launched), and a
+// cudaGraphSetConditional costs ~1 us of the single-CTA decide: set a
+// handle only when its value changes (Ctrl::cond mirrors the handles).
+__device__ __forceinline__ void set_cond_if_changed(const Params& P, Ctrl& C, int bit,
+                                                    cudaGraphConditionalHandle h, unsigned v) {
+  const int cur = (C.cond >> bit) & 1;
+  if (cur != (int)v) {
+    set_cond(P, h, v);
+    C.cond ^= 1 << bit;
+  }
 }
 
 // Sum of v[0..count) in a fixed order: sequential (the reference's order)
@@ -1522,10 +1833,15 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
       C.at_cap = C.total_k >= P.max_it;
       C.check = (C.total_k % P.period == 0) || C.at_cap;
       const int nba = (C.active + P.W - 1) / P.W;
-      C.Rp = rounds_adjust(items_per_block(P.n, P.m, P.W, P.grid, nba, P.l2_budget), nba,
-                           P.grid_run);
-      C.Rd = rounds_adjust(items_per_block(P.m, P.n, P.W, P.grid, nba, P.l2_budget), nba,
-                           P.grid_run);
+      if (P.r_tab) {  // the same rule, tabulated per active block count on the host
+        C.Rp = P.r_tab[nba];
+        C.Rd = P.r_tab[P.Kp / P.W + 1 + nba];
+      } else {
+        C.Rp = rounds_adjust(items_per_block(P.n, P.m, P.W, P.grid, nba, P.l2_budget), nba,
+                             P.grid_run);
+        C.Rd = rounds_adjust(items_per_block(P.m, P.n, P.W, P.grid, nba, P.l2_budget), nba,
+                             P.grid_run);
+      }
       C.Rc = C.Rp;
     }
     C.cert_pending = 0;
@@ -1534,10 +1850,10 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
     const double state_bytes =
         8.0 * (double)((C.active + P.W - 1) / P.W) * P.W * (double)(P.n + P.m);
     const bool handover = P.handover_bytes > 0.0 && state_bytes < P.handover_bytes;
-    set_cond(P, P.h_loop, (C.done || handover) ? 0u : 1u);
-    set_cond(P, P.h_check, (!C.done && C.check) ? 1u : 0u);
-    set_cond(P, P.h_snap, (C.n_snap > 0 || C.n_moves > 0) ? 1u : 0u);
-    if (P.trace) set_cond(P, P.h_trace, C.hash_pending ? 1u : 0u);
+    set_cond_if_changed(P, C, CB_LOOP, P.h_loop, (C.done || handover) ? 0u : 1u);
+    set_cond_if_changed(P, C, CB_CHECK, P.h_check, (!C.done && C.check) ? 1u : 0u);
+    set_cond_if_changed(P, C, CB_SNAP, P.h_snap, (C.n_snap > 0 || C.n_moves > 0) ? 1u : 0u);
+    if (P.trace) set_cond_if_changed(P, C, CB_TRACE, P.h_trace, C.hash_pending ? 1u : 0u);
   }
   decide_mark(P, plain, 22);
 }
@@ -1614,12 +1930,12 @@ static __device__ void decide_body(const Params& P, int phase) {
         C.error = ish[3] == 2 ? BL_ERR_LOGIC : BL_ERR_DOMAIN;
         if (P.prof) atomicMax(&P.prof[2 * K_DECIDE + 1], gtime());
         C.done = 1;
+        set_cond_if_changed(P, C, CB_LOOP, P.h_loop, 0u);
+        set_cond_if_changed(P, C, CB_CHECK, P.h_check, 0u);
+        set_cond_if_changed(P, C, CB_CERT, P.h_cert, 0u);
+        set_cond_if_changed(P, C, CB_SNAP, P.h_snap, 0u);
+        if (P.trace) set_cond_if_changed(P, C, CB_TRACE, P.h_trace, 0u);
         *P.ctrl = C;
-        set_cond(P, P.h_loop, 0u);
-        set_cond(P, P.h_check, 0u);
-        set_cond(P, P.h_cert, 0u);
-        set_cond(P, P.h_snap, 0u);
-        if (P.trace) set_cond(P, P.h_trace, 0u);
       }
       return;
     }
@@ -1661,14 +1977,14 @@ static __device__ void decide_body(const Params& P, int phase) {
           C.sparse_products += ish[0];
           C.cert_pending = 1;
           C.launches += 2;
+          set_cond_if_changed(P, C, CB_CERT, P.h_cert, 1u);
           *P.ctrl = C;
-          set_cond(P, P.h_cert, 1u);
           if (P.prof) atomicMax(&P.prof[2 * K_DECIDE + 1], gtime());
         }
         return;
       }
     }
-    if (tid == 0) set_cond(P, P.h_cert, 0u);
+    if (tid == 0) set_cond_if_changed(P, C, CB_CERT, P.h_cert, 0u);
   } else {
     mean = C.mean;
     for (int j = tid; j < active; j += (int)blockDim.x) {
@@ -2494,6 +2810,7 @@ __global__ void __launch_bounds__(kBlock) k_loop(Params P, int tail_smem) {
 // ---------------------------------------------------------------------------
 struct PiOp {
   static constexpr int V = 2;
+  static constexpr int kStreams = 0;
   const int *rp, *ci;
   const double *cv, *in;
   double* out;

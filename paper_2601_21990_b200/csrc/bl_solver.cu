@@ -108,7 +108,7 @@ struct bl_ctx {
     B_SLOTD, B_SLOTI, B_ORIGI, B_RES, B_COLSUM, B_PART, B_CNT, B_SNAP, B_MOVES,
     B_LOG, B_CTRL, B_PROF, B_PROFACC, B_BAR, B_OV, B_OVD, B_WARMX, B_WARMY, B_PI, B_TMP0, B_TMP1,
     B_TUNE0, B_TUNE1, B_TUNE2, B_TUNE3,
-    B_TAIL, B_DBG, B_SPART, B_SCNT, B_COUNT
+    B_TAIL, B_DBG, B_SPART, B_SCNT, B_RTAB, B_COUNT
   };
   DevBuf buf[B_COUNT];
   // last solve
@@ -852,6 +852,19 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.grid_run = use_graph ? ctx->sms * bl::plain_ctas_per_sm(W) : 0;
   if (std::getenv("BATCHLP_NO_ROUNDS")) P.grid_run = 0;
   P.l2_budget = l2_budget;
+  {  // the decide kernel's work-item geometry per active block count
+    std::vector<int> tab(2 * ((size_t)nb + 1));
+    for (int nba = 0; nba <= nb; ++nba) {
+      tab[nba] = bl::rounds_adjust(bl::items_per_block(n, m, W, P.grid, nba, l2_budget), nba,
+                                   P.grid_run);
+      tab[nb + 1 + nba] = bl::rounds_adjust(bl::items_per_block(m, n, W, P.grid, nba, l2_budget),
+                                            nba, P.grid_run);
+    }
+    int* dtab = static_cast<int*>(ctx->buf[bl_ctx::B_RTAB].ensure(sizeof(int) * tab.size()));
+    ck(cudaMemcpyAsync(dtab, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice, s),
+       "geometry table");
+    P.r_tab = dtab;
+  }
   P.handover_bytes = (mode_loop == 0) ? kHandoverBytes : 0.0;
   // TMA-gather kernels for W = 32 (bl_tma.cuh), opt-in with BATCHLP_TMA=1:
   // measured slower than the register-gather kernels on B200 (the TMA unit's
@@ -950,6 +963,7 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   c0.at_cap = 0 >= cfg.max_iterations;
   c0.check = 1;
   c0.anchor_reset = 1;
+  c0.cond = bl::kCondDefaults;  // the graph handles' defaults at launch
   {
     const int nba = (active + W - 1) / W;
     c0.Rp = bl::rounds_adjust(bl::items_per_block(n, m, W, P.grid, nba, l2_budget), nba,

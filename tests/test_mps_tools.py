@@ -49,7 +49,7 @@ def test_mps_fsb_and_bench_match_reference(tmp_path, ref):
     _require(DROPIN)
     import paper_2601_21990_b200 as bl
     from paper_2601_21990_b200 import instances as I
-    rows, cols, dens, seed = 150, 300, 0.04, 5
+    rows, cols, dens, seed = 250, 500, 0.02, 3  # 10 fractional root columns
     mps = tmp_path / "setcover.mps"
     subprocess.run([DROPIN, "--write-mps", str(rows), str(cols), str(dens), str(seed),
                     str(mps)], check=True)
