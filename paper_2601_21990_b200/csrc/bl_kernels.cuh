@@ -137,54 +137,6 @@ __device__ __forceinline__ void ld_gather(const double* p, double (&o)[V]) {
   }
 }
 
-// ---- cp.async staging of the streamed operands ----------------------------
-// Each lane copies its own V doubles of a row's streamed operands (X, aX in
-// the primal; Y, AX, aY, aAX in the dual) into shared memory one row ahead,
-// so their latency overlaps the current row's gathers without holding
-// registers: the registers go to deeper gather batches instead. A lane only
-// reads back what it copied itself, so cp.async.wait_group is the only sync.
-#ifndef BL_STAGE
-#define BL_STAGE 1
-#endif
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ unsigned long long policy_evict_first() {
-  unsigned long long pol;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-template <int V>
-__device__ __forceinline__ void cp_stream(double* dst, const double* src) {
-  const unsigned long long pol = policy_evict_first();
-  if constexpr (V == 2)
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
-                 :: "r"(smem_addr(dst)), "l"(src), "l"(pol) : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;"
-                 :: "r"(smem_addr(dst)), "l"(src), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory");
-}
-template <int V>
-__device__ __forceinline__ void ld_stage(const double* p, double (&o)[V]) {
-  if constexpr (V == 2) {
-    const double2 t = *reinterpret_cast<const double2*>(p);
-    o[0] = t.x;
-    o[1] = t.y;
-  } else {
-    o[0] = *p;
-  }
-}
-// lane tid's copy of streamed operand k in stage st
-template <int V, int NOPS>
-__device__ __forceinline__ double* stage_slot(double* stg, int st, int k) {
-  return stg + ((size_t)(st * NOPS + k) * kBlock + threadIdx.x) * V;
-}
-
 // One CSR row of op(A) times the lane's V slots of a column block. The
 // accumulation follows the stored order with separately rounded products
 // and sums: the reference csr_apply (sparse.hpp:176-183) bit for bit.
@@ -339,55 +291,6 @@ __device__ __forceinline__ void gather_row_grp(const int* __restrict__ rp,
   }
 }
 
-// The cooperative product with D gathers in flight per batch (D = 8 when
-// the streamed operands are staged in shared memory and the registers are
-// free): one metadata round trip per L nonzeros, ceil(cnt / D) gather round
-// trips. Same summation order.
-#ifndef BL_GATHER_DEPTH
-#define BL_GATHER_DEPTH 8
-#endif
-template <int W, int D>
-__device__ __forceinline__ void gather_row_deep(const int* __restrict__ rp,
-                                                const int* __restrict__ ci,
-                                                const double* __restrict__ cv,
-                                                const double* __restrict__ base, int i, int L,
-                                                double (&acc)[Geo<W>::V]) {
-  constexpr int V = Geo<W>::V;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & (L - 1);
-  const unsigned mask = L >= 32 ? 0xffffffffu : (((1u << L) - 1u) << (lane & ~(L - 1)));
-  const int p = __ldg(rp + i);
-  const int e = __ldg(rp + i + 1);
-#pragma unroll
-  for (int v = 0; v < V; ++v) acc[v] = 0.0;
-  for (int ch = p; ch < e; ch += L) {
-    const int k = ch + gl;
-    int myc = 0;
-    double myv = 0.0;
-    if (k < e) {
-      myc = __ldg(ci + k);
-      myv = __ldg(cv + k);
-    }
-    const int cnt = min(L, e - ch);
-    for (int t = 0; t < cnt; t += D) {
-      double x[D][V];
-#pragma unroll
-      for (int q = 0; q < D; ++q) {
-        const int c = __shfl_sync(mask, myc, t + q, L);
-        if (t + q < cnt) ld_gather<V>(base + (size_t)c * W, x[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < D; ++q) {
-        const double a = __shfl_sync(mask, myv, t + q, L);
-        if (t + q < cnt) {
-#pragma unroll
-          for (int v = 0; v < V; ++v) acc[v] = __dadd_rn(acc[v], __dmul_rn(a, x[q][v]));
-        }
-      }
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // deterministic per-column reduction of one work item
 // ---------------------------------------------------------------------------
@@ -523,7 +426,14 @@ __device__ __forceinline__ void set_lanes(Op& op, int L) {
 #ifndef BL_DYNAMIC_ITEMS
 #define BL_DYNAMIC_ITEMS 1
 #endif
-template <int W, int NS, int LL = 0, bool STG = false, class Op>
+// REV: walk the column blocks last to first. The dual runs reversed so it
+// starts on the block whose XT the primal wrote last, and the next primal
+// (forward) starts on the block whose Y the dual wrote last: each pass
+// begins on operands still in L2.
+#ifndef BL_PINGPONG
+#define BL_PINGPONG 1
+#endif
+template <int W, int NS, int LL = 0, bool REV = false, class Op>
 __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
                                          double* partials, int* counters,
                                          double* colsum, int s0, int Kp, double* red,
@@ -535,7 +445,8 @@ __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
   const int items = nb * R;
   const int per = R > 0 ? (rows + R - 1) / R : 0;
   auto item = [&](int w) {
-    const int b = w / R, r = w - b * R;
+    const int bw = w / R, r = w - bw * R;
+    const int b = (REV && BL_PINGPONG) ? nb - 1 - bw : bw;
     const int r0 = min(rows, r * per), r1 = min(rows, r0 + per);
     const int cnt = r1 - r0;
     int gs, ge;
@@ -557,22 +468,7 @@ __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
     __syncthreads();
     op.begin(b, slot0, acc, r == 0 && g == 0, &s_col[li * V]);
     set_lanes(op, L);
-    if constexpr (STG && BL_STAGE && Op::kStreams > 0) {
-      // row i's streamed operands were copied while row i - 1 ran
-      if (gs < ge) op.prefetch(b, gs, li, red, 0);
-      cp_commit();
-      for (int i = gs; i < ge; ++i) {
-        const int st = (i - gs) & 1;
-        if (i + 1 < ge) op.prefetch(b, i + 1, li, red, st ^ 1);
-        cp_commit();
-        cp_wait<1>();
-        op.row_staged(b, i, li, acc, red, st);
-      }
-      cp_wait<0>();
-      __syncthreads();  // the staging ring is the reduction scratch
-    } else {
-      for (int i = gs; i < ge; ++i) op.row(b, i, slot0, li, acc);
-    }
+    for (int i = gs; i < ge; ++i) op.row(b, i, slot0, li, acc);
     publish_item<W, NS, LL>(acc, b, r, R, partials, counters, colsum, s0, Kp, red);
   };
   if (!BL_DYNAMIC_ITEMS || ticket == nullptr) {
@@ -731,53 +627,28 @@ __device__ __forceinline__ void stage_col(const Params& P, int j, int active, bo
 // primal: XT = proj(X - tau (c + A'Y)), X' = Halpern, sums
 // ---------------------------------------------------------------------------
 // GEN: the CSR arrays may be the tail's shared-memory cache (generic loads)
-template <int W, bool CHECK, bool GEN = false, bool LAZY = false>
+template <int W, bool CHECK, bool GEN = false>
 struct PrimalOp {
   static constexpr int V = Geo<W>::V;
   const Params& P;
   int active, reset;
   double alpha, oma;
-  const double *Ycur, *Xcur;
-  double* Xnxt;
+  int cur;  // X / Y buffer of this iteration (pointers come from P: no registers)
   const volatile SColInfo* col;  // this lane's V column descriptors (shared memory)
   const int* crp;                // A' CSR (global, or a shared-memory cache of it)
   const int* cci;
   const double* ccv;
   int lanes = Geo<W>::L;  // lanes per row group (narrow tail mappings use fewer)
-  // LAZY (the staged graph kernels): the control block lives in the CTA's
-  // shared memory and every per-launch scalar / pointer is re-read from it
-  // or from the kernel parameters where it is used, so none of them pins
-  // a register across the gather loop.
-  const Ctrl* lc = nullptr;
-  __device__ __forceinline__ int reset_() const {
-    if constexpr (LAZY) return lc->anchor_reset; else return reset;
+  __device__ __forceinline__ const int* rp_() const {
+    if constexpr (GEN) return crp; else return P.trp;
   }
-  __device__ __forceinline__ double alpha_() const {
-    if constexpr (LAZY) return lc->alpha; else return alpha;
+  __device__ __forceinline__ const int* ci_() const {
+    if constexpr (GEN) return cci; else return P.tci;
   }
-  __device__ __forceinline__ double oma_() const {
-    if constexpr (LAZY) return 1.0 - lc->alpha; else return oma;
-  }
-  __device__ __forceinline__ const double* Ycur_() const {
-    if constexpr (LAZY) return P.Y[lc->cur]; else return Ycur;
-  }
-  __device__ __forceinline__ const double* Xcur_() const {
-    if constexpr (LAZY) return P.X[lc->cur]; else return Xcur;
-  }
-  __device__ __forceinline__ double* Xnxt_() const {
-    if constexpr (LAZY) return P.X[lc->cur ^ 1]; else return Xnxt;
-  }
-  __device__ __forceinline__ const int* crp_() const {
-    if constexpr (LAZY) return P.trp; else return crp;
-  }
-  __device__ __forceinline__ const int* cci_() const {
-    if constexpr (LAZY) return P.tci; else return cci;
-  }
-  __device__ __forceinline__ const double* ccv_() const {
-    if constexpr (LAZY) return P.tcv; else return ccv;
+  __device__ __forceinline__ const double* cv_() const {
+    if constexpr (GEN) return ccv; else return P.tcv;
   }
   __device__ PrimalOp(const Params& p, const Ctrl& C) : P(p) {
-    if constexpr (LAZY) lc = &C;
     crp = P.trp;
     cci = P.tci;
     ccv = P.tcv;
@@ -785,42 +656,11 @@ struct PrimalOp {
     reset = C.anchor_reset;
     alpha = C.alpha;
     oma = 1.0 - alpha;
-    Ycur = P.Y[C.cur];
-    Xcur = P.X[C.cur];
-    Xnxt = P.X[C.cur ^ 1];
+    cur = C.cur;
   }
   __device__ void stage(int j, volatile SColInfo* s) { stage_col(P, j, active, false, s); }
   __device__ void begin(int, int, double (&)[2][V], bool, const volatile SColInfo* sc) {
     col = sc;
-  }
-  // streamed operands staged through shared memory (not for the tail's
-  // cached-metadata rows, which run their own schedule)
-  static constexpr int kStreams = GEN ? 0 : 2;
-  __device__ void prefetch(int b, int i, int li, double* stg, int st) {
-    const size_t idx = ((size_t)b * P.n + i) * W + li * V;
-    cp_stream<V>(stage_slot<V, 2>(stg, st, 0), Xcur_() + idx);
-    if (!reset_()) cp_stream<V>(stage_slot<V, 2>(stg, st, 1), P.aX + idx);
-  }
-  __device__ void row_staged(int b, int i, int li, double (&acc)[2][V], const double* stg,
-                             int st) {
-    const int n = P.n, m = P.m;
-    const double bc = P.mode == BL_SHARED_OBJECTIVE ? __ldg(P.c + i) : 0.0;
-    const double bl = __ldg(P.xl + i), bh = __ldg(P.xu + i);
-    const size_t idx = ((size_t)b * n + i) * W + li * V;
-    double aty[V];
-    if (lanes >= 8)
-      gather_row_deep<W, BL_GATHER_DEPTH>(crp_(), cci_(), ccv_(), Ycur_() + (size_t)b * m * W + li * V, i, lanes, aty);
-    else
-      gather_row<W>(crp_(), cci_(), ccv_(), Ycur_() + (size_t)b * m * W + li * V, i, aty);
-    double x[V], ax[V];
-    ld_stage<V>(stage_slot<V, 2>(const_cast<double*>(stg), st, 0), x);
-    if (reset_()) {
-#pragma unroll
-      for (int v = 0; v < V; ++v) ax[v] = x[v];
-    } else {
-      ld_stage<V>(stage_slot<V, 2>(const_cast<double*>(stg), st, 1), ax);
-    }
-    finish(idx, i, bc, bl, bh, x, ax, aty, acc);
   }
   __device__ __forceinline__ void finish(size_t idx, int i, double bc, double bl, double bh,
                                          const double (&x)[V], const double (&ax)[V],
@@ -844,12 +684,12 @@ struct PrimalOp {
         acc[0][v] += dx * dx;
         acc[1][v] += da * da;
       }
-      xn[v] = alpha_() * (2.0 * xt[v] - x[v]) + oma_() * ax[v];
+      xn[v] = alpha * (2.0 * xt[v] - x[v]) + oma * ax[v];
       if (CHECK) rc[v] = project_barrier(-cc - aty[v], lo, hi);
     }
     st_wb<V>(P.XT + idx, xt);
-    st_cs<V>(Xnxt_() + idx, xn);
-    if (reset_()) st_cs<V>(P.aX + idx, x);
+    st_cs<V>(P.X[cur ^ 1] + idx, xn);
+    if (reset) st_cs<V>(P.aX + idx, x);
     if (CHECK) st_wb<V>(P.RC + idx, rc);
   }
   __device__ void row(int b, int i, int, int li, double (&acc)[2][V]) {
@@ -859,8 +699,8 @@ struct PrimalOp {
     const double bl = __ldg(P.xl + i), bh = __ldg(P.xu + i);
     const size_t idx = ((size_t)b * n + i) * W + li * V;
     double x[V], ax[V];
-    ld_cs<V>(Xcur_() + idx, x);
-    if (reset_()) {
+    ld_cs<V>(P.X[cur] + idx, x);
+    if (reset) {
 #pragma unroll
       for (int v = 0; v < V; ++v) ax[v] = x[v];
     } else {
@@ -868,20 +708,17 @@ struct PrimalOp {
     }
     double aty[V];
     // (the cooperative-metadata gather measured slower for A' rows: short rows)
-    gather_row<W, GEN>(crp_(), cci_(), ccv_(), Ycur_() + (size_t)b * m * W + li * V, i, aty);
+    gather_row<W, GEN>(rp_(), ci_(), cv_(), P.Y[cur] + (size_t)b * m * W + li * V, i, aty);
     finish(idx, i, bc, bl, bh, x, ax, aty, acc);
   }
 };
 
-// STG: stage the streamed operands through `red` (kRowSmemDoubles; the
-// graph's row kernels). The persistent / cluster loop kernels keep the
-// register path (their static shared memory has no room for the ring).
-template <int W, bool CHECK, int LL = 0, bool STG = false>
+template <int W, bool CHECK, int LL = 0>
 static __device__ void primal_body(const Params& P, const Ctrl& C, double* red) {
   prof_begin(P, K_PRIMAL);
-  PrimalOp<W, CHECK, false, STG> op(P, C);  // STG: C is in shared memory
+  PrimalOp<W, CHECK> op(P, C);
   const int nb = (C.active + W - 1) / W;
-  run_rows<W, 2, LL, STG>(op, P.n, nb, C.Rp, P.partials, P.counters, P.colsum, S_DX2, P.Kp, red,
+  run_rows<W, 2, LL>(op, P.n, nb, C.Rp, P.partials, P.counters, P.colsum, S_DX2, P.Kp, red,
                      P.ticket);
   prof_end(P, K_PRIMAL);
 }
@@ -893,73 +730,48 @@ static __device__ void primal_body(const Params& P, const Ctrl& C, double* red) 
 #endif
 template <int W, bool CHECK>
 __global__ void __launch_bounds__(kBlock, kPrimalMinCtas) k_primal(Params P) {
-  __shared__ __align__(16) double red[kRowSmemDoubles];
+  __shared__ double red[kRedDoubles];
   __shared__ Ctrl C;  // shared: the staged row ops re-read it per row
   if (threadIdx.x == 0) C = *P.ctrl;
   __syncthreads();
   if (C.done) return;
   if constexpr (BL_NARROW_ROWS && W >= 16) {
     const int Lsel = pass_lanes<W>(C.active);
-    BL_DISPATCH_L(W, Lsel, (primal_body<W, CHECK, LL_, true>(P, C, red)));
+    BL_DISPATCH_L(W, Lsel, (primal_body<W, CHECK, LL_>(P, C, red)));
   } else {
-    primal_body<W, CHECK, 0, true>(P, C, red);
+    primal_body<W, CHECK>(P, C, red);
   }
 }
 
 // ---------------------------------------------------------------------------
 // dual: AXT = A XT, YT = sigma (s - proj(s)), Y'/AX' = Halpern, sums
 // ---------------------------------------------------------------------------
-template <int W, bool CHECK, bool GRP = true, bool GEN = false, bool LAZY = false>
+#ifndef BL_DUAL_LATE
+#define BL_DUAL_LATE 1
+#endif
+template <int W, bool CHECK, bool GRP = true, bool GEN = false>
 struct DualOp {
   static constexpr int V = Geo<W>::V;
   static constexpr int NS = CHECK ? 9 : 3;
   const Params& P;
   int active, reset;
   double alpha, oma;
-  const double *Ycur, *AXcur;
-  double *Ynxt, *AXnxt;
+  int cur;  // Y / AX buffer of this iteration (pointers come from P)
   const volatile SColInfo* col;
   const int* crp;  // A CSR (global, or a shared-memory cache of it)
   const int* cci;
   const double* ccv;
   int lanes = Geo<W>::L;
-  // LAZY (the staged graph kernels): the control block lives in the CTA's
-  // shared memory and every per-launch scalar / pointer is re-read from it
-  // or from the kernel parameters where it is used, so none of them pins
-  // a register across the gather loop.
-  const Ctrl* lc = nullptr;
-  __device__ __forceinline__ int reset_() const {
-    if constexpr (LAZY) return lc->anchor_reset; else return reset;
+  __device__ __forceinline__ const int* rp_() const {
+    if constexpr (GEN) return crp; else return P.rp;
   }
-  __device__ __forceinline__ double alpha_() const {
-    if constexpr (LAZY) return lc->alpha; else return alpha;
+  __device__ __forceinline__ const int* ci_() const {
+    if constexpr (GEN) return cci; else return P.ci;
   }
-  __device__ __forceinline__ double oma_() const {
-    if constexpr (LAZY) return 1.0 - lc->alpha; else return oma;
-  }
-  __device__ __forceinline__ const double* Ycur_() const {
-    if constexpr (LAZY) return P.Y[lc->cur]; else return Ycur;
-  }
-  __device__ __forceinline__ const double* AXcur_() const {
-    if constexpr (LAZY) return P.AX[lc->cur]; else return AXcur;
-  }
-  __device__ __forceinline__ double* Ynxt_() const {
-    if constexpr (LAZY) return P.Y[lc->cur ^ 1]; else return Ynxt;
-  }
-  __device__ __forceinline__ double* AXnxt_() const {
-    if constexpr (LAZY) return P.AX[lc->cur ^ 1]; else return AXnxt;
-  }
-  __device__ __forceinline__ const int* crp_() const {
-    if constexpr (LAZY) return P.rp; else return crp;
-  }
-  __device__ __forceinline__ const int* cci_() const {
-    if constexpr (LAZY) return P.ci; else return cci;
-  }
-  __device__ __forceinline__ const double* ccv_() const {
-    if constexpr (LAZY) return P.cv; else return ccv;
+  __device__ __forceinline__ const double* cv_() const {
+    if constexpr (GEN) return ccv; else return P.cv;
   }
   __device__ DualOp(const Params& p, const Ctrl& C) : P(p) {
-    if constexpr (LAZY) lc = &C;
     crp = P.rp;
     cci = P.ci;
     ccv = P.cv;
@@ -967,73 +779,40 @@ struct DualOp {
     reset = C.anchor_reset;
     alpha = C.alpha;
     oma = 1.0 - alpha;
-    Ycur = P.Y[C.cur];
-    AXcur = P.AX[C.cur];
-    Ynxt = P.Y[C.cur ^ 1];
-    AXnxt = P.AX[C.cur ^ 1];
+    cur = C.cur;
   }
   __device__ void stage(int j, volatile SColInfo* s) { stage_col(P, j, active, true, s); }
   __device__ void begin(int, int, double (&)[NS][V], bool, const volatile SColInfo* sc) {
     col = sc;
-  }
-  static constexpr int kStreams = GEN ? 0 : 4;
-  __device__ void prefetch(int b, int i, int li, double* stg, int st) {
-    const size_t idx = ((size_t)b * P.m + i) * W + li * V;
-    cp_stream<V>(stage_slot<V, 4>(stg, st, 0), Ycur_() + idx);
-    cp_stream<V>(stage_slot<V, 4>(stg, st, 1), AXcur_() + idx);
-    if (!reset_()) {
-      cp_stream<V>(stage_slot<V, 4>(stg, st, 2), P.aY + idx);
-      cp_stream<V>(stage_slot<V, 4>(stg, st, 3), P.aAX + idx);
-    }
-  }
-  __device__ void row_staged(int b, int i, int li, double (&acc)[NS][V], const double* stg,
-                             int st) {
-    const int n = P.n, m = P.m;
-    const double lo = __ldg(P.rl + i), hi = __ldg(P.ru + i);
-    const size_t idx = ((size_t)b * m + i) * W + li * V;
-    double axt[V];
-    if (lanes >= 8)
-      gather_row_deep<W, BL_GATHER_DEPTH>(crp_(), cci_(), ccv_(), P.XT + (size_t)b * n * W + li * V, i, lanes, axt);
-    else
-      gather_row<W>(crp_(), cci_(), ccv_(), P.XT + (size_t)b * n * W + li * V, i, axt);
-    double* sg = const_cast<double*>(stg);
-    double y[V], ax[V], ay[V], aax[V];
-    ld_stage<V>(stage_slot<V, 4>(sg, st, 0), y);
-    ld_stage<V>(stage_slot<V, 4>(sg, st, 1), ax);
-    if (reset_()) {
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        ay[v] = y[v];
-        aax[v] = ax[v];
-      }
-    } else {
-      ld_stage<V>(stage_slot<V, 4>(sg, st, 2), ay);
-      ld_stage<V>(stage_slot<V, 4>(sg, st, 3), aax);
-    }
-    finish(idx, lo, hi, y, ax, ay, aax, axt, acc);
   }
   __device__ void row(int b, int i, int, int li, double (&acc)[NS][V]) {
     const int n = P.n, m = P.m;
     const double lo = __ldg(P.rl + i), hi = __ldg(P.ru + i);
     const size_t idx = ((size_t)b * m + i) * W + li * V;
     double y[V], ax[V], ay[V], aax[V];
-    ld_cs<V>(Ycur_() + idx, y);
-    ld_cs<V>(AXcur_() + idx, ax);
-    if (reset_()) {
+    auto streams = [&]() {
+      ld_cs<V>(P.Y[cur] + idx, y);
+      ld_cs<V>(P.AX[cur] + idx, ax);
+      if (reset) {
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        ay[v] = y[v];
-        aax[v] = ax[v];
+        for (int v = 0; v < V; ++v) {
+          ay[v] = y[v];
+          aax[v] = ax[v];
+        }
+      } else {
+        ld_cs<V>(P.aY + idx, ay);
+        ld_cs<V>(P.aAX + idx, aax);
       }
-    } else {
-      ld_cs<V>(P.aY + idx, ay);
-      ld_cs<V>(P.aAX + idx, aax);
-    }
+    };
+    // BL_DUAL_LATE: request the streamed operands after the gather, so they
+    // hold no registers while it runs (the dual's live set spills otherwise)
+    if (!BL_DUAL_LATE || GEN) streams();
     double axt[V];
-    if (GEN) gather_row<W, true>(crp_(), cci_(), ccv_(), P.XT + (size_t)b * n * W + li * V, i, axt);
+    if (GEN) gather_row<W, true>(rp_(), ci_(), cv_(), P.XT + (size_t)b * n * W + li * V, i, axt);
     else if (GRP && lanes >= 4)
-      gather_row_grp<W>(crp_(), cci_(), ccv_(), P.XT + (size_t)b * n * W + li * V, i, lanes, axt);
-    else gather_row<W>(crp_(), cci_(), ccv_(), P.XT + (size_t)b * n * W + li * V, i, axt);
+      gather_row_grp<W>(rp_(), ci_(), cv_(), P.XT + (size_t)b * n * W + li * V, i, lanes, axt);
+    else gather_row<W>(rp_(), ci_(), cv_(), P.XT + (size_t)b * n * W + li * V, i, axt);
+    if (BL_DUAL_LATE && !GEN) streams();
     finish(idx, lo, hi, y, ax, ay, aax, axt, acc);
   }
   __device__ __forceinline__ void finish(size_t idx, double lo, double hi, const double (&y)[V],
@@ -1048,7 +827,7 @@ struct DualOp {
       const int valid = sc->valid;
       // dual_step_element, solver.hpp:186-190
       const double vv = 2.0 * axt[v] - ax[v];
-      const double s = y[v] / sigma + vv;
+      const double s = div_by_step(y[v], sigma) + vv;
       yt[v] = sigma * (s - project_box(s, lo, hi));
       const double dy = yt[v] - y[v];
       const double da = y[v] - ay[v];
@@ -1057,8 +836,8 @@ struct DualOp {
         acc[1][v] += dy * (axt[v] - ax[v]);
         acc[2][v] += da * da;
       }
-      yn[v] = alpha_() * (2.0 * yt[v] - y[v]) + oma_() * ay[v];
-      axn[v] = alpha_() * (2.0 * axt[v] - ax[v]) + oma_() * aax[v];
+      yn[v] = alpha * (2.0 * yt[v] - y[v]) + oma * ay[v];
+      axn[v] = alpha * (2.0 * axt[v] - ax[v]) + oma * aax[v];
       if constexpr (CHECK) {
         dyb[v] = project_barrier(yt[v] - y[v], lo, hi);
         if (valid) {
@@ -1075,9 +854,9 @@ struct DualOp {
         }
       }
     }
-    st_cs<V>(Ynxt_() + idx, yn);
-    st_cs<V>(AXnxt_() + idx, axn);
-    if (reset_()) {
+    st_cs<V>(P.Y[cur ^ 1] + idx, yn);
+    st_cs<V>(P.AX[cur ^ 1] + idx, axn);
+    if (reset) {
       st_cs<V>(P.aY + idx, y);
       st_cs<V>(P.aAX + idx, ax);
     }
@@ -1089,28 +868,28 @@ struct DualOp {
   }
 };
 
-template <int W, bool CHECK, int LL = 0, bool GRP = true, bool STG = false>
+template <int W, bool CHECK, int LL = 0, bool GRP = true>
 static __device__ void dual_body(const Params& P, const Ctrl& C, double* red) {
   prof_begin(P, K_DUAL);
-  DualOp<W, CHECK, GRP, false, STG> op(P, C);  // STG: C is in shared memory
+  DualOp<W, CHECK, GRP> op(P, C);
   const int nb = (C.active + W - 1) / W;
-  run_rows<W, DualOp<W, CHECK, GRP, false, STG>::NS, LL, STG>(op, P.m, nb, C.Rd, P.partials, P.counters,
+  run_rows<W, DualOp<W, CHECK, GRP>::NS, LL, true>(op, P.m, nb, C.Rd, P.partials, P.counters,
                                     P.colsum, S_DY2, P.Kp, red, P.ticket);
   prof_end(P, K_DUAL);
 }
 
 template <int W, bool CHECK>
 __global__ void __launch_bounds__(kBlock, kDualMinCtas) k_dual(Params P) {
-  __shared__ __align__(16) double red[kRowSmemDoubles];
+  __shared__ double red[kRedDoubles];
   __shared__ Ctrl C;  // shared: the staged row ops re-read it per row
   if (threadIdx.x == 0) C = *P.ctrl;
   __syncthreads();
   if (C.done) return;
   if constexpr (BL_NARROW_ROWS && W >= 16) {
     const int Lsel = pass_lanes<W>(C.active);
-    BL_DISPATCH_L(W, Lsel, (dual_body<W, CHECK, LL_, true, true>(P, C, red)));
+    BL_DISPATCH_L(W, Lsel, (dual_body<W, CHECK, LL_>(P, C, red)));
   } else {
-    dual_body<W, CHECK, 0, true, true>(P, C, red);
+    dual_body<W, CHECK>(P, C, red);
   }
 }
 
@@ -1120,7 +899,6 @@ __global__ void __launch_bounds__(kBlock, kDualMinCtas) k_dual(Params P) {
 template <int W>
 struct CheckOp {
   static constexpr int V = Geo<W>::V;
-  static constexpr int kStreams = 0;
   static constexpr int NS = 10;
   const Params& P;
   int active;
@@ -1222,7 +1000,6 @@ __global__ void __launch_bounds__(kBlock, kRowMinCtas) k_check(Params P) {
 template <int W>
 struct CertOp {
   static constexpr int V = Geo<W>::V;
-  static constexpr int kStreams = 0;
   const Params& P;
   int active;
   int flag[V];
@@ -1275,7 +1052,6 @@ __global__ void __launch_bounds__(kBlock, kRowMinCtas) k_cert(Params P) {
 template <int W>
 struct SpmmOp {
   static constexpr int V = Geo<W>::V;
-  static constexpr int kStreams = 0;
   const int *rp, *ci;
   const double *cv, *in;
   double* out;
@@ -2810,7 +2586,6 @@ __global__ void __launch_bounds__(kBlock) k_loop(Params P, int tail_smem) {
 // ---------------------------------------------------------------------------
 struct PiOp {
   static constexpr int V = 2;
-  static constexpr int kStreams = 0;
   const int *rp, *ci;
   const double *cv, *in;
   double* out;
@@ -2882,10 +2657,6 @@ inline int grid_of(const void* fn) {
 
 #ifdef BL_WLAUNCH_DEFINE
 }  // namespace bl
-#ifdef BL_WITH_TMA
-#include "bl_tma.cuh"
-#include "bl_slice.cuh"
-#endif
 namespace bl {
 
 template <int W>
@@ -2897,53 +2668,6 @@ void WLaunch<W>::iteration_check(const Params& P, cudaStream_t s) {
 
 template <int W>
 void WLaunch<W>::iteration_plain(const Params& P, cudaStream_t s) {
-#ifdef BL_WITH_TMA
-  if constexpr (W == 32) {
-    if (P.slice_p.ch > 0) {  // slice-staged kernels (bl_slice.cuh)
-      static int grid = 0;
-      if (grid == 0) {
-        const int mx = 227 * 1024 - 6144;
-        cudaFuncSetAttribute(k_slice<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_slice<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid = sms;
-      }
-      if (P.slice_p.stages == 0) {
-        static bool attr = false;
-        if (!attr) {
-          const int mx = 227 * 1024 - 8192;
-          cudaFuncSetAttribute(k_slice_direct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-          cudaFuncSetAttribute(k_slice_direct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-          attr = true;
-        }
-        k_slice_direct<false><<<grid, kSliceDirectThreads, P.slice_p.smem, s>>>(P);
-        k_slice_direct<true><<<grid, kSliceDirectThreads, P.slice_d.smem, s>>>(P);
-      } else {
-        k_slice<false><<<grid, P.slice_p.ch * kSliceLanes, P.slice_p.smem, s>>>(P);
-        k_slice<true><<<grid, P.slice_d.ch * kSliceLanes, P.slice_d.smem, s>>>(P);
-      }
-      return;
-    }
-    if (P.tma_host) {  // TMA-gather kernels (bl_tma.cuh)
-      static int grid = 0;
-      if (grid == 0) {
-        cudaFuncSetAttribute(k_primal_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-        cudaFuncSetAttribute(k_dual_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-        int dev = 0, sms = 148, occ = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_primal_tma, kTmaThreads, kTmaSmem);
-        grid = sms * (occ < 1 ? 1 : occ);
-      }
-      const TmaMaps& M = *static_cast<const TmaMaps*>(P.tma_host);
-      k_primal_tma<<<grid, kTmaThreads, kTmaSmem, s>>>(P, M);
-      k_dual_tma<<<grid, kTmaThreads, kTmaSmem, s>>>(P, M);
-      return;
-    }
-  }
-#endif
   k_primal<W, false><<<grid_of((const void*)k_primal<W, false>), kBlock, 0, s>>>(P);
   k_dual<W, false><<<grid_of((const void*)k_dual<W, false>), kBlock, 0, s>>>(P);
 }

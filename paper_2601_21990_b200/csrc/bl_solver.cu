@@ -11,9 +11,7 @@
 //   host is not consulted between iterations; it reads the control block
 //   once at the end.
 
-#include <cuda.h>
 #include <cuda_runtime.h>
-#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -30,13 +28,6 @@
 #include "batchlp_cuda.h"
 #include "bl_device.cuh"
 
-namespace bl {
-// must match bl_tma.cuh
-struct TmaMaps {
-  CUtensorMap y[2], ax[2], x[2], xt, anx, any, anax;
-};
-
-}  // namespace bl
 
 namespace {
 
@@ -108,7 +99,7 @@ struct bl_ctx {
     B_SLOTD, B_SLOTI, B_ORIGI, B_RES, B_COLSUM, B_PART, B_CNT, B_SNAP, B_MOVES,
     B_LOG, B_CTRL, B_PROF, B_PROFACC, B_BAR, B_OV, B_OVD, B_WARMX, B_WARMY, B_PI, B_TMP0, B_TMP1,
     B_TUNE0, B_TUNE1, B_TUNE2, B_TUNE3,
-    B_TAIL, B_DBG, B_SPART, B_SCNT, B_RTAB, B_COUNT
+    B_TAIL, B_DBG, B_RTAB, B_COUNT
   };
   DevBuf buf[B_COUNT];
   // last solve
@@ -123,7 +114,6 @@ struct bl_ctx {
   bl::Params exec_params{};
   int exec_trace = -1;
   bl::Ctrl* h_ctrl = nullptr;  // pinned
-  bl::TmaMaps maps{};          // TMA descriptors of the current solve's state
   // tail graph cache
   cudaGraphExec_t tail_exec = nullptr;
   cudaGraph_t tail_graph = nullptr;
@@ -204,7 +194,7 @@ int items_for(int rows, int W, int grid) {
 
 template <class T>
 void upload(DevBuf& b, const T* src, size_t count, cudaStream_t s) {
-  b.ensure(count * sizeof(T) + 16);  // the slice kernels copy aligned 16-byte supersets
+  b.ensure(count * sizeof(T) + 16);
   if (count) ck(cudaMemcpyAsync(b.p, src, count * sizeof(T), cudaMemcpyHostToDevice, s),
                 "upload");
 }
@@ -310,82 +300,6 @@ int tail_smem_bytes(const bl_problem* p, int cl) {
     worst = std::max(worst, bytes);
   }
   return worst <= (size_t)160 * 1024 ? (int)((worst + 15) / 16 * 16) : 0;
-}
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no
-// libcuda link dependency).
-PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-// [rows][32] fp64 tile view of a column-block-tiled matrix, one 256-byte row
-// per box (gather4 moves four such boxes).
-bool tile_map(CUtensorMap* m, const double* base, size_t rows, unsigned box_cols = 32,
-              unsigned box_rows = 1) {
-  auto fn = encode_tiled();
-  if (!fn || rows == 0 || rows > 0xffffffffull) return false;
-  cuuint64_t dims[2] = {32, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {256};
-  cuuint32_t box[2] = {box_cols, box_rows};
-  cuuint32_t es[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// Geometry of a slice kernel over `rows` CSR rows (row pointers `h`) that
-// gathers from `rows_in` rows, streaming `na` arrays: the largest chunk that
-// leaves >= 3 pipeline stages in shared memory (else >= 2), the nonzero
-// capacity of any chunk-sized row window (bl_slice.cuh).
-// BATCHLP_SLICE: 0 = register-gather kernels (default), 1 = staged slice
-// kernels, 2 = direct slice kernels.
-int slice_mode() {
-  const char* e = std::getenv("BATCHLP_SLICE");
-  return e ? std::atoi(e) : 0;
-}
-
-bool slice_geometry(bool direct, int na, int rows, int rows_in, const std::vector<int>& h,
-                    bl::SliceGeo* g) {
-  if (direct) {  // sub-slice + row pointers only (stages = 0)
-    const int bytes = bl::slice_bytes(rows_in) + bl::slice_rp_bytes(rows);
-    if (bytes > 227 * 1024 - 8192) return false;
-    *g = bl::SliceGeo{1, 0, 0, bytes};
-    return true;
-  }
-  constexpr int kMaxDyn = 227 * 1024 - 6144;  // minus the kernels' static shared memory
-  const int avail = kMaxDyn - bl::slice_bytes(rows_in) - bl::slice_rp_bytes(rows);
-  if (avail <= 0 || (int)h.size() != rows + 1) return false;
-  int force = 0;
-  if (const char* e = std::getenv("BATCHLP_SLICE_CH")) force = std::atoi(e);
-  int force_st = 0;
-  if (const char* e = std::getenv("BATCHLP_SLICE_STAGES")) force_st = std::atoi(e);
-  for (int need = 3; need >= 2; --need) {
-    for (int ch : {128, 96, 64, 32}) {
-      if (force && ch != force) continue;
-      int nz = 0;
-      for (int i = 0; i < rows; ++i) nz = std::max(nz, h[std::min(rows, i + ch)] - h[i]);
-      nz = (nz + 3) & ~3;
-      const int sb = bl::slice_stage_bytes(na, ch, nz);
-      int st = std::min(bl::kSliceMaxStages, avail / sb);
-      if (force_st) st = std::min(st, force_st);
-      if (st >= need || (force && st >= 2)) {
-        *g = bl::SliceGeo{ch, st, nz, bl::slice_bytes(rows_in) + bl::slice_rp_bytes(rows) + st * sb};
-        return true;
-      }
-    }
-  }
-  return false;
 }
 
 void free_graph(bl_ctx* ctx) {
@@ -795,7 +709,18 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   // per-block fold counters, then the row kernels' work-item ticket
   P.counters = static_cast<int*>(
       ctx->buf[bl_ctx::B_CNT].ensure(sizeof(int) * ((size_t)std::max(nb, 64) + 2)));
-  P.ticket = P.counters + std::max(nb, 64);
+  // Block-major dynamic work items pay off once one column block's gathered
+  // operand is a sizeable share of L2 (C4: -21% per row pass, measured); on
+  // small problems the per-item atomics cost more than the drift they
+  // prevent (C2: +15%), so they use the static stride.
+  {
+    static const double min_bytes = [] {
+      const char* e = std::getenv("BATCHLP_TICKET_MIN_BYTES");
+      return e ? std::atof(e) : 4.0 * (1 << 20);
+    }();
+    const double block_operand = 8.0 * W * (double)std::max(m, n);
+    P.ticket = block_operand >= min_bytes ? P.counters + std::max(nb, 64) : nullptr;
+  }
   P.snap_list = static_cast<int*>(ctx->buf[bl_ctx::B_SNAP].ensure(sizeof(int) * 3 * (size_t)Kp));
   P.moves = static_cast<int*>(ctx->buf[bl_ctx::B_MOVES].ensure(sizeof(int) * 2 * (size_t)Kp));
   P.log_cap = 1 << 16;
@@ -866,45 +791,6 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
     P.r_tab = dtab;
   }
   P.handover_bytes = (mode_loop == 0) ? kHandoverBytes : 0.0;
-  // TMA-gather kernels for W = 32 (bl_tma.cuh), opt-in with BATCHLP_TMA=1:
-  // measured slower than the register-gather kernels on B200 (the TMA unit's
-  // per-instruction cost dominates 256-byte gathers)
-  P.tma_host = nullptr;
-  {
-    const char* e = std::getenv("BATCHLP_TMA");
-    const bool want = W == 32 && e && e[0] == '1';
-    if (want) {
-      const size_t rn = (size_t)nb * n, rm = (size_t)nb * m;
-      bl::TmaMaps& M = ctx->maps;
-      bool ok = rn > 0 && rm > 0;
-      for (int k = 0; k < 2 && ok; ++k) {
-        ok = ok && tile_map(&M.y[k], P.Y[k], rm) && tile_map(&M.ax[k], P.AX[k], rm) &&
-             tile_map(&M.x[k], P.X[k], rn);
-      }
-      ok = ok && tile_map(&M.xt, P.XT, rn) && tile_map(&M.anx, P.aX, rn) &&
-           tile_map(&M.any, P.aY, rm) && tile_map(&M.anax, P.aAX, rm);
-      if (ok) P.tma_host = &ctx->maps;
-    }
-  }
-  // slice-staged kernels for W = 32 when an 8-slot sub-slice of either
-  // gathered operand fits in shared memory (bl_slice.cuh), opt-in with
-  // BATCHLP_SLICE=1: measured slower than the register-gather kernels on B200
-  // (one 210 KB CTA per SM leaves 2-3 warps per scheduler)
-  P.slice_part = nullptr;
-  P.slice_cnt = nullptr;
-  P.slice_p = P.slice_d = bl::SliceGeo{0, 0, 0, 0};
-  if (W == 32 && !P.tma_host && m <= bl::kSliceMaxRows && n <= bl::kSliceMaxRows && m > 0 &&
-      n > 0 && slice_mode() > 0 &&
-      slice_geometry(slice_mode() == 2, 2, n, m, p->h_trp, &P.slice_p) &&
-      slice_geometry(slice_mode() == 2, 4, m, n, p->h_rp, &P.slice_d)) {
-    const int nvb = Kp / bl::kSliceCols;
-    P.slice_part = static_cast<double*>(ctx->buf[bl_ctx::B_SPART].ensure(
-        sizeof(double) * (size_t)nvb * bl::kSliceRMax * 3 * bl::kSliceCols));
-    P.slice_cnt = static_cast<int*>(ctx->buf[bl_ctx::B_SCNT].ensure(sizeof(int) * (size_t)nvb));
-    ck(cudaMemsetAsync(P.slice_cnt, 0, sizeof(int) * (size_t)nvb, s), "slice counters");
-  } else {
-    P.slice_p = P.slice_d = bl::SliceGeo{0, 0, 0, 0};
-  }
   P.tail_part = static_cast<double*>(
       ctx->buf[bl_ctx::B_TAIL].ensure(sizeof(double) * 16 * 5 * 32));
   if (std::getenv("BATCHLP_NO_FAST_TAIL")) P.tail_part = nullptr;

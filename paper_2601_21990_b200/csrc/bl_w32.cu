@@ -2,7 +2,6 @@
 // their launchers (one translation unit per width so the build runs in
 // parallel).
 #define BL_WLAUNCH_DEFINE
-#define BL_WITH_TMA
 #include "bl_kernels.cuh"
 
 namespace bl {

@@ -126,51 +126,3 @@ def test_loop_drivers_agree_with_reference_c1(ref, loop, monkeypatch):
         assert abs(br.down_objective - want["down_objective"][j]) <= 1e-6 * (1 + abs(want["down_objective"][j]))
         assert abs(br.up_iterations - want["up_iterations"][j]) <= 0.1 * want["up_iterations"][j]
         assert abs(br.down_iterations - want["down_iterations"][j]) <= 0.1 * want["down_iterations"][j]
-
-
-def test_tma_gather_kernels_agree_with_reference_c2_prefix(ref, monkeypatch):
-    """The opt-in TMA gather4 kernels (bl_tma.cuh) compute the same plain
-    passes: C2 OBBT capped at 256 iterations matches the reference."""
-    monkeypatch.setenv("BATCHLP_TMA", "1")
-    monkeypatch.setenv("BATCHLP_LOOP", "graph")
-    p = I.config_problem("c2")
-    ob = bl.build_obbt_batch(p, bl.ObbtConfig())
-    cfg = bl.ObbtConfig().solver_config()
-    cfg.max_iterations = 256
-    got = bl.solve_batch(ob.batch, cfg, ob.presets, vectors=bl.Vectors.NONE)
-    want = ref.solve_batch(p, ob.batch.batch_width(), 1, [], cfg,
-                           [(q.column, int(q.result.status), q.result.objective)
-                            for q in ob.presets], vectors=False)
-    assert got.iterations == want.iterations
-    for g, w in zip(got.per_problem, want.per_problem):
-        assert int(g.status) == w.status
-        assert abs(g.iterations - w.iterations) <= 0.1 * max(w.iterations, 1)
-        if w.status == 0:
-            assert abs(g.objective - w.objective) <= 1e-6 * (1 + abs(w.objective))
-
-
-@pytest.mark.parametrize("geometry", ["direct", "auto", "128/2", "64/4", "32/2"])
-def test_slice_kernels_agree_with_reference_c2_prefix(ref, geometry, monkeypatch):
-    """The slice kernels (bl_slice.cuh: 8-slot operand sub-slice in shared
-    memory; direct, or with pipelined row chunks at several chunk / stage
-    geometries): C2 OBBT capped at 256 iterations matches the reference."""
-    monkeypatch.setenv("BATCHLP_LOOP", "graph")
-    monkeypatch.setenv("BATCHLP_SLICE", "2" if geometry == "direct" else "1")
-    if geometry not in ("auto", "direct"):
-        ch, st = geometry.split("/")
-        monkeypatch.setenv("BATCHLP_SLICE_CH", ch)
-        monkeypatch.setenv("BATCHLP_SLICE_STAGES", st)
-    p = I.config_problem("c2")
-    ob = bl.build_obbt_batch(p, bl.ObbtConfig())
-    cfg = bl.ObbtConfig().solver_config()
-    cfg.max_iterations = 256
-    got = bl.solve_batch(ob.batch, cfg, ob.presets, vectors=bl.Vectors.NONE)
-    want = ref.solve_batch(p, ob.batch.batch_width(), 1, [], cfg,
-                           [(q.column, int(q.result.status), q.result.objective)
-                            for q in ob.presets], vectors=False)
-    assert got.iterations == want.iterations
-    for g, w in zip(got.per_problem, want.per_problem):
-        assert int(g.status) == w.status
-        assert abs(g.iterations - w.iterations) <= 0.1 * max(w.iterations, 1)
-        if w.status == 0:
-            assert abs(g.objective - w.objective) <= 1e-6 * (1 + abs(w.objective))
