@@ -184,11 +184,16 @@ void launch_init(const Params& P, cudaStream_t s, const double* warm_x,
 
 void launch_spmm(const Params& P, cudaStream_t s, bool transpose, const double* in,
                  double* out, int active) {
-  const int rows = transpose ? P.n : P.m;
+  const int rows = transpose ? P.n : P.m, rows_in = transpose ? P.m : P.n;
   BL_DISPATCH_W(P.W, {
     constexpr int G = Geo<W_>::G;
-    int R = rows <= kTinyRows ? 1 : (rows + 2 * G - 1) / (2 * G);
-    if (R > P.grid) R = P.grid;
+    int R;
+    if (P.l2_budget > 0) {  // the row kernels' L2-aware decomposition
+      R = items_per_block(rows, rows_in, W_, P.grid, (active + W_ - 1) / W_, P.l2_budget);
+    } else {
+      R = rows <= kTinyRows ? 1 : (rows + 2 * G - 1) / (2 * G);
+      if (R > P.grid) R = P.grid;
+    }
     if (R < 1) R = 1;
     WLaunch<W_>::spmm(P, s, transpose, in, out, active, R);
   });

@@ -292,17 +292,51 @@ __device__ __forceinline__ void gather_row_grp(const int* __restrict__ rp,
 }
 
 // ---------------------------------------------------------------------------
+// column sums and the M-norm residual
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double cs(const Params& P, int s, int j) {
+  return P.colsum[(size_t)s * P.Kp + j];
+}
+__device__ __forceinline__ double& csr(const Params& P, int s, int j) {
+  return P.colsum[(size_t)s * P.Kp + j];
+}
+
+// m_residual_from_terms, solver.hpp:250-263
+__device__ __forceinline__ double m_residual(double dx2, double dy2, double cross,
+                                             double eta, double w, int* err) {
+  const double msq = (w / eta) * dx2 + (1.0 / (eta * w)) * dy2 + 2.0 * cross;
+  if (msq < 0.0) {
+    const double scale = (w / eta) * dx2 + (1.0 / (eta * w)) * dy2 + 2.0 * fabs(cross);
+    if (msq < -1e-12 * smax(1.0, scale)) *err = 1;
+    return 0.0;
+  }
+  return sqrt(msq);
+}
+
+// ---------------------------------------------------------------------------
 // deterministic per-column reduction of one work item
 // ---------------------------------------------------------------------------
 // acc[s][v]: this lane's sums for slots (b*W + li*V + v). Reduces over the
 // CTA in a fixed tree, writes the item's partials, and the last CTA of block
 // b folds all R partials in item order into colsum[s0+s][slot].
 // `red` is a shared buffer of at least kRedDoubles doubles.
-template <int W, int NS, int LL = 0>
+// Ops may finish a column block once its sums are folded (only ops with an
+// after_fold member; called by the CTA that folded, after a barrier).
+template <class Op>
+__device__ __forceinline__ auto after_fold_impl(Op& op, int b, int) -> decltype(op.after_fold(b), void()) {
+  __syncthreads();  // the fold's colsum stores are visible to the whole CTA
+  op.after_fold(b);
+}
+template <class Op>
+__device__ __forceinline__ void after_fold_impl(Op&, int, long) {}
+
+struct NoOp {};
+
+template <int W, int NS, int LL = 0, class Op = NoOp>
 __device__ __forceinline__ void publish_item(double (&acc)[NS][Geo<W>::V], int b,
                                              int r, int R, double* partials,
                                              int* counters, double* colsum,
-                                             int s0, int Kp, double* red) {
+                                             int s0, int Kp, double* red, Op* op = nullptr) {
   using Gm = Geo<W, LL>;
   constexpr int V = Gm::V, L = Gm::L;
   static_assert(kWarps * NS * W <= kRedDoubles, "reduction buffer too small");
@@ -374,6 +408,7 @@ __device__ __forceinline__ void publish_item(double (&acc)[NS][Geo<W>::V], int b
       }
     }
     if (tid == 0) counters[b] = 0;
+    if (op) after_fold_impl(*op, b, 0);
   }
   __syncthreads();
 }
@@ -469,7 +504,7 @@ __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
     op.begin(b, slot0, acc, r == 0 && g == 0, &s_col[li * V]);
     set_lanes(op, L);
     for (int i = gs; i < ge; ++i) op.row(b, i, slot0, li, acc);
-    publish_item<W, NS, LL>(acc, b, r, R, partials, counters, colsum, s0, Kp, red);
+    publish_item<W, NS, LL>(acc, b, r, R, partials, counters, colsum, s0, Kp, red, &op);
   };
   if (!BL_DYNAMIC_ITEMS || ticket == nullptr) {
     for (int w = blockIdx.x; w < items; w += gridDim.x) item(w);
@@ -785,6 +820,26 @@ struct DualOp {
   __device__ void begin(int, int, double (&)[NS][V], bool, const volatile SColInfo* sc) {
     col = sc;
   }
+  // Once block b's dual sums are folded (the primal's are final since the
+  // previous launch), its M-norm residuals (m_residual_from_terms,
+  // solver.hpp:250-263) and their sequential block sum are computed here,
+  // so the single-CTA decide only combines block sums (batch_solver.hpp:
+  // 209-222). Warp 0 does it: W <= 32 slots.
+  __device__ void after_fold(int b) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x, j = b * W + lane;
+    double r = 0.0;
+    if (lane < W && j < active) {
+      int err = 0;
+      r = m_residual(cs(P, S_DX2, j), cs(P, S_DY2, j), cs(P, S_CROSS, j), P.eta, P.w[j], &err);
+      P.resid[j] = r;
+      if (err) atomicOr(P.err_flag, 1);
+    }
+    double sum = 0.0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) sum += __shfl_sync(0xffffffffu, r, k);
+    if (lane == 0) P.blk_resid[b] = sum;
+  }
   __device__ void row(int b, int i, int, int li, double (&acc)[NS][V]) {
     const int n = P.n, m = P.m;
     const double lo = __ldg(P.rl + i), hi = __ldg(P.ru + i);
@@ -1088,31 +1143,12 @@ __global__ void __launch_bounds__(kBlock) k_spmm(Params P, int transpose,
   op.active = active;
   const int nb = (active + W - 1) / W;
   __shared__ double red[kRedDoubles];
-  run_rows<W, 1>(op, op.rows_out, nb, R, partials, counters, colsum, 0, P.Kp, red);
+  run_rows<W, 1>(op, op.rows_out, nb, R, partials, counters, colsum, 0, P.Kp, red, P.ticket);
 }
 
 // ---------------------------------------------------------------------------
 // decide: one CTA runs the batch control of batch_solver.hpp:203-345
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double cs(const Params& P, int s, int j) {
-  return P.colsum[(size_t)s * P.Kp + j];
-}
-__device__ __forceinline__ double& csr(const Params& P, int s, int j) {
-  return P.colsum[(size_t)s * P.Kp + j];
-}
-
-// m_residual_from_terms, solver.hpp:250-263
-__device__ __forceinline__ double m_residual(double dx2, double dy2, double cross,
-                                             double eta, double w, int* err) {
-  const double msq = (w / eta) * dx2 + (1.0 / (eta * w)) * dy2 + 2.0 * cross;
-  if (msq < 0.0) {
-    const double scale = (w / eta) * dx2 + (1.0 / (eta * w)) * dy2 + 2.0 * fabs(cross);
-    if (msq < -1e-12 * smax(1.0, scale)) *err = 1;
-    return 0.0;
-  }
-  return sqrt(msq);
-}
-
 // ---- correctly rounded exp / log (double-double) ---------------------------
 // The weight update is the only transcendental on the path. glibc's exp/log
 // return the correctly rounded value except in rare near-midpoint cases, so
@@ -1686,20 +1722,10 @@ static __device__ void decide_body(const Params& P, int phase) {
       if (C.passes > 2 * P.max_it + 1024) ish[3] = 2;
     }
     __syncthreads();
-    // residuals; for a wide batch the strided partial sums of ordered_sum are
-    // accumulated on the fly (same order), saving a reload of resid
+    // The residuals were computed by the dual kernel's per-block folds
+    // (DualOp::after_fold); a broken metric raised err_flag there.
     const int count = P.avg_all ? P.width : active;
-    const bool fused_sum = !P.avg_all && count > 256;
-    double part = 0.0;
-#pragma unroll 4
-    for (int j = tid; j < active; j += (int)blockDim.x) {
-      int err = 0;
-      const double r = m_residual(cs(P, S_DX2, j), cs(P, S_DY2, j), cs(P, S_CROSS, j),
-                                  P.eta, P.w[j], &err);
-      P.resid[j] = r;
-      part += r;
-      if (err) ish[3] = 1;
-    }
+    if (tid == 0 && *reinterpret_cast<volatile int*>(P.err_flag)) ish[3] = 1;
     __syncthreads();
     if (ish[3]) {
       if (tid == 0) {
@@ -1715,17 +1741,13 @@ static __device__ void decide_body(const Params& P, int phase) {
       }
       return;
     }
-    if (fused_sum) {
-      sh[tid] = part;
-      __syncthreads();
-      for (int off = (int)blockDim.x / 2; off > 0; off >>= 1) {
-        if (tid < off) sh[tid] = sh[tid] + sh[tid + off];
-        __syncthreads();
-      }
-      mean = sh[0] / (double)count;
-      __syncthreads();
-    } else {
+    // Averaged residual (batch_solver.hpp:209-222): up to 256 terms, the
+    // reference's sequential sum in slot order; a wider batch adds the
+    // column blocks' sequential sums in block order.
+    if (count <= 256 || P.avg_all) {
       mean = ordered_sum(P.resid, count, sh) / (double)count;
+    } else {
+      mean = ordered_sum(P.blk_resid, (active + P.W - 1) / P.W, sh) / (double)count;
     }
     decide_mark(P, plain_pass, 11);
     if (C.inner_k == 0) {

@@ -615,8 +615,8 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
     P.RDY = static_cast<double*>(ctx->buf[bl_ctx::B_RDY].ensure(sizeof(double) * (size_t)width * m));
     P.RDR = static_cast<double*>(ctx->buf[bl_ctx::B_RDR].ensure(sizeof(double) * (size_t)width * n));
   }
-  // per-slot doubles: w resid anchor best*9 t*6 scratch = 19 arrays
-  constexpr int kSlotD = 19;
+  // per-slot doubles: w resid anchor best*9 t*6 scratch blk_resid = 20 arrays
+  constexpr int kSlotD = 20;
   double* sd = static_cast<double*>(ctx->buf[bl_ctx::B_SLOTD].ensure(sizeof(double) * kSlotD * (size_t)Kp));
   P.w = sd;
   P.resid = sd + 1 * (size_t)Kp;
@@ -637,6 +637,7 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.t_score = sd + 16 * (size_t)Kp;
   P.t_dsup = sd + 17 * (size_t)Kp;
   P.scratch = sd + 18 * (size_t)Kp;
+  P.blk_resid = sd + 19 * (size_t)Kp;  // one per column block (<= Kp)
   constexpr int kSlotI = 7;
   int* si = static_cast<int*>(ctx->buf[bl_ctx::B_SLOTI].ensure(sizeof(int) * kSlotI * (size_t)Kp));
   P.slot_orig = si;
@@ -645,6 +646,8 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.cert_flag = si + 3 * (size_t)Kp;
   P.move_src = si + 4 * (size_t)Kp;
   P.snap_orig = si + 5 * (size_t)Kp;
+  P.err_flag = si + 6 * (size_t)Kp;
+  ck(cudaMemsetAsync(P.err_flag, 0, sizeof(int), s), "err flag");
   int* oi = static_cast<int*>(ctx->buf[bl_ctx::B_ORIGI].ensure(sizeof(int) * 3 * (size_t)width));
   P.orig_done = oi;
   P.ov_beg = oi + width;
@@ -987,6 +990,25 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
 // C-ABI
 // ===========================================================================
 namespace {
+// Work decomposition of a standalone SpMM (bl_spmm, bl_csr_apply, the
+// tuner): the row kernels' L2-aware items per block and, when one column
+// block's operand is large, block-major dynamic work items (as in a solve);
+// partials sized for either orientation.
+void spmm_geometry(bl_ctx* ctx, bl::Params& P, int nb, int rows, int rows_in, int W,
+                   cudaStream_t s) {
+  P.l2_budget = 16ll << 20;
+  size_t R = (size_t)std::max(items_for(rows, W, ctx->grid), items_for(rows_in, W, ctx->grid));
+  R = std::max(R, (size_t)bl::items_per_block(rows, rows_in, W, ctx->grid, nb, P.l2_budget));
+  R = std::max(R, (size_t)bl::items_per_block(rows_in, rows, W, ctx->grid, nb, P.l2_budget));
+  P.partials = static_cast<double*>(
+      ctx->buf[bl_ctx::B_PART].ensure(sizeof(double) * (size_t)nb * R * 10 * W));
+  const size_t nc = (size_t)std::max(nb, 64) + 2;
+  P.counters = static_cast<int*>(ctx->buf[bl_ctx::B_CNT].ensure(sizeof(int) * nc));
+  ck(cudaMemsetAsync(P.counters, 0, sizeof(int) * nc, s), "counters");
+  const double block_operand = 8.0 * W * (double)std::max(rows, rows_in);
+  P.ticket = block_operand >= 4.0 * (1 << 20) ? P.counters + std::max(nb, 64) : nullptr;
+}
+
 // op(A) x for the first `active` of `width` column-major host columns:
 // tiles them, runs the SpMM kernel, untiles, copies back (bl_spmm,
 // bl_csr_apply).
@@ -1018,10 +1040,7 @@ void device_spmm(bl_ctx* ctx, const bl_problem* p, bool transpose, int width, in
   P.Kp = Kp;
   P.grid = ctx->grid;
   const int nb = Kp / W;
-  const int R = items_for(rout, W, ctx->grid);
-  P.partials = static_cast<double*>(ctx->buf[bl_ctx::B_PART].ensure(sizeof(double) * (size_t)nb * R * 10 * W));
-  P.counters = static_cast<int*>(ctx->buf[bl_ctx::B_CNT].ensure(sizeof(int) * (size_t)std::max(nb, 64)));
-  ck(cudaMemsetAsync(P.counters, 0, sizeof(int) * (size_t)std::max(nb, 64), s), "counters");
+  spmm_geometry(ctx, P, nb, rout, rin, W, s);
   P.colsum = static_cast<double*>(ctx->buf[bl_ctx::B_COLSUM].ensure(sizeof(double) * bl::S_COUNT * (size_t)Kp));
   bl::launch_spmm(P, s, transpose, tin, tout, active);
   bl::launch_from_tiled(s, tout, raw, rout, width, W, active);
@@ -1265,11 +1284,7 @@ int bl_measure_spmm(bl_ctx* ctx, const bl_problem* p, int32_t width, int32_t rep
     P.Kp = Kp;
     P.grid = ctx->grid;
     const int nb = Kp / W;
-    const int R = std::max(items_for(m, W, ctx->grid), items_for(n, W, ctx->grid));
-    P.partials = static_cast<double*>(
-        ctx->buf[bl_ctx::B_PART].ensure(sizeof(double) * (size_t)nb * R * 10 * W));
-    P.counters = static_cast<int*>(ctx->buf[bl_ctx::B_CNT].ensure(sizeof(int) * (size_t)std::max(nb, 64)));
-    ck(cudaMemsetAsync(P.counters, 0, sizeof(int) * (size_t)std::max(nb, 64), s), "counters");
+    spmm_geometry(ctx, P, nb, m, n, W, s);
     P.colsum = static_cast<double*>(
         ctx->buf[bl_ctx::B_COLSUM].ensure(sizeof(double) * bl::S_COUNT * (size_t)Kp));
     for (int warm = 0; warm < 2; ++warm) {
