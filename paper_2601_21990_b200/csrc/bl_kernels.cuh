@@ -458,9 +458,76 @@ __device__ __forceinline__ void set_lanes(Op& op, int L) {
 // Walks the work items of a persistent row kernel. Op provides:
 //   begin(b, slot0, acc, owner)  per item (owner: holds the matrix's row 0)
 //   row(b, i, slot0, acc)        per row of the group's contiguous chunk
+// One work item: rows [r * per, (r + 1) * per) of column block b, split
+// over the CTA's row groups (a tiny dimension is walked by one group), then
+// the item's deterministic reduction (publish_item).
+template <int W, int NS, int LL = 0, class Op>
+__device__ __forceinline__ void run_item(Op& op, int b, int r, int rows, int R,
+                                         double* partials, int* counters, double* colsum,
+                                         int s0, int Kp, double* red) {
+  using Gm = Geo<W, LL>;
+  constexpr int V = Gm::V, L = Gm::L, G = Gm::G;
+  SColInfo* s_col = col_smem();
+  const int tid = threadIdx.x, g = tid / L, li = tid - g * L;
+  const int per = R > 0 ? (rows + R - 1) / R : 0;
+  const int r0 = min(rows, r * per), r1 = min(rows, r0 + per);
+  const int cnt = r1 - r0;
+  int gs, ge;
+  if (rows <= kTinyRows) {  // whole dimension tiny: one sequential walk
+    gs = g == 0 ? r0 : r1;
+    ge = r1;
+  } else {
+    const int ch = (cnt + G - 1) / G;
+    gs = min(r1, r0 + g * ch);
+    ge = min(r1, gs + ch);
+  }
+  double acc[NS][V];
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[s][v] = 0.0;
+  const int slot0 = b * W + li * V;
+  if (tid < W) op.stage(b * W + tid, &s_col[tid]);
+  __syncthreads();
+  op.begin(b, slot0, acc, r == 0 && g == 0, &s_col[li * V]);
+  set_lanes(op, L);
+  for (int i = gs; i < ge; ++i) op.row(b, i, slot0, li, acc);
+  publish_item<W, NS, LL>(acc, b, r, R, partials, counters, colsum, s0, Kp, red, &op);
+}
+
 #ifndef BL_DYNAMIC_ITEMS
 #define BL_DYNAMIC_ITEMS 1
 #endif
+// Items [0, items) handed to the grid from one atomic ticket, in order (the
+// next one fetched while the current item runs), so every CTA works on the
+// column block the grid is on: only ~one block's gathered operand is live in
+// L2 (a static stride lets slow and fast CTAs drift apart by blocks). Which
+// CTA runs an item changes no sum: partials are indexed by item and folded
+// in item order. The last CTA to retire re-arms the ticket (and runs
+// `on_last`, thread 0) for the next launch / phase.
+template <class F, class G>
+__device__ __forceinline__ void ticket_items(int* ticket, int items, F&& fn, G&& on_last) {
+  const int tid = threadIdx.x;
+  __shared__ int s_next[2];
+  if (tid == 0) s_next[0] = atomicAdd(ticket, 1);
+  __syncthreads();
+  int par = 0;
+  for (int w = s_next[0]; w < items; w = s_next[par]) {
+    if (tid == 0) s_next[par ^ 1] = atomicAdd(ticket, 1);
+    fn(w);  // ends with a CTA barrier: s_next[par ^ 1] is visible
+    par ^= 1;
+  }
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(ticket + 1, 1) == (int)gridDim.x - 1) {
+      on_last();
+      atomicExch(ticket, 0);
+      atomicExch(ticket + 1, 0);
+      __threadfence();
+    }
+  }
+}
+
 // REV: walk the column blocks last to first. The dual runs reversed so it
 // starts on the block whose XT the primal wrote last, and the next primal
 // (forward) starts on the block whose Y the dual wrote last: each pass
@@ -473,67 +540,17 @@ __device__ __forceinline__ void run_rows(Op& op, int rows, int nb, int R,
                                          double* partials, int* counters,
                                          double* colsum, int s0, int Kp, double* red,
                                          int* ticket = nullptr) {
-  using Gm = Geo<W, LL>;
-  constexpr int V = Gm::V, L = Gm::L, G = Gm::G;
-  SColInfo* s_col = col_smem();
-  const int tid = threadIdx.x, g = tid / L, li = tid - g * L;
   const int items = nb * R;
-  const int per = R > 0 ? (rows + R - 1) / R : 0;
   auto item = [&](int w) {
     const int bw = w / R, r = w - bw * R;
     const int b = (REV && BL_PINGPONG) ? nb - 1 - bw : bw;
-    const int r0 = min(rows, r * per), r1 = min(rows, r0 + per);
-    const int cnt = r1 - r0;
-    int gs, ge;
-    if (rows <= kTinyRows) {  // whole dimension tiny: one sequential walk
-      gs = g == 0 ? r0 : r1;
-      ge = r1;
-    } else {
-      const int ch = (cnt + G - 1) / G;
-      gs = min(r1, r0 + g * ch);
-      ge = min(r1, gs + ch);
-    }
-    double acc[NS][V];
-#pragma unroll
-    for (int s = 0; s < NS; ++s)
-#pragma unroll
-      for (int v = 0; v < V; ++v) acc[s][v] = 0.0;
-    const int slot0 = b * W + li * V;
-    if (tid < W) op.stage(b * W + tid, &s_col[tid]);
-    __syncthreads();
-    op.begin(b, slot0, acc, r == 0 && g == 0, &s_col[li * V]);
-    set_lanes(op, L);
-    for (int i = gs; i < ge; ++i) op.row(b, i, slot0, li, acc);
-    publish_item<W, NS, LL>(acc, b, r, R, partials, counters, colsum, s0, Kp, red, &op);
+    run_item<W, NS, LL>(op, b, r, rows, R, partials, counters, colsum, s0, Kp, red);
   };
   if (!BL_DYNAMIC_ITEMS || ticket == nullptr) {
     for (int w = blockIdx.x; w < items; w += gridDim.x) item(w);
     return;
   }
-  // Items handed out in block-major order from one atomic ticket (the next
-  // one fetched while the current item runs): every CTA stays on the column
-  // block the grid is working on, so only ~one block's gathered operand is
-  // live in L2 (a static stride lets slow and fast CTAs drift apart by
-  // blocks). Which CTA runs an item does not change any sum: partials are
-  // indexed by item and folded in item order.
-  __shared__ int s_next[2];
-  if (tid == 0) s_next[0] = atomicAdd(ticket, 1);
-  __syncthreads();
-  int par = 0;
-  for (int w = s_next[0]; w < items; w = s_next[par]) {
-    if (tid == 0) s_next[par ^ 1] = atomicAdd(ticket, 1);
-    item(w);  // ends with a CTA barrier: s_next[par ^ 1] is visible
-    par ^= 1;
-  }
-  // the last CTA to retire re-arms the ticket for the next launch / phase
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(ticket + 1, 1) == (int)gridDim.x - 1) {
-      atomicExch(ticket, 0);
-      atomicExch(ticket + 1, 0);
-      __threadfence();
-    }
-  }
+  ticket_items(ticket, items, item, [] {});
 }
 
 // Lanes per row for a pass: full width unless one block is active, then the
@@ -946,6 +963,59 @@ __global__ void __launch_bounds__(kBlock, kDualMinCtas) k_dual(Params P) {
   } else {
     dual_body<W, CHECK>(P, C, red);
   }
+}
+
+// ---------------------------------------------------------------------------
+// fused plain pass: per column block, the primal items then the dual items
+// ---------------------------------------------------------------------------
+// One launch walks (block b: Rp primal items, then Rd dual items) in ticket
+// order; a CTA that draws a dual item of block b waits until all of b's
+// primal items are done (their XT rows written, their sums folded). The dual
+// then gathers XT(b) and streams Y(b) while the primal has just written /
+// gathered them, instead of one whole-K pass later when they left L2 (C4:
+// the separate dual reads 1.86x its algorithmic DRAM bytes). Sums, order of
+// operations and results are those of k_primal followed by k_dual.
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBlock, kDualMinCtas) k_pass(Params P) {
+  __shared__ double red[kRedDoubles];
+  __shared__ Ctrl C;
+  if (threadIdx.x == 0) C = *P.ctrl;
+  __syncthreads();
+  if (C.done) return;
+  prof_begin(P, K_PASS);
+  const int nb = (C.active + W - 1) / W;
+  const int Rp = C.Rp, Rd = C.Rd, per = Rp + Rd;
+  int* pdone = P.pdone;
+  auto item = [&](int w) {
+    const int b = w / per, k = w - b * per;
+    if (k < Rp) {
+      PrimalOp<W, false> op(P, C);
+      run_item<W, 2>(op, b, k, P.n, Rp, P.partials, P.counters, P.colsum, S_DX2, P.Kp, red);
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(pdone + b, 1);
+      }
+    } else {
+      if (threadIdx.x == 0) {
+        while (ld_acquire_gpu(pdone + b) < Rp) __nanosleep(128);
+        __threadfence();  // (gpu scope: also drops stale L1 lines before the XT gathers)
+      }
+      __syncthreads();
+      DualOp<W, false> op(P, C);
+      run_item<W, DualOp<W, false>::NS>(op, b, k - Rp, P.m, Rd, P.partials + P.part_stride,
+                                        P.counters + P.cnt_stride, P.colsum, S_DY2, P.Kp, red);
+    }
+  };
+  ticket_items(P.ticket, nb * per, item, [&] {
+    for (int b = 0; b < nb; ++b) pdone[b] = 0;
+  });
+  prof_end(P, K_PASS);
 }
 
 // ---------------------------------------------------------------------------
@@ -1666,6 +1736,9 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
     set_cond_if_changed(P, C, CB_CHECK, P.h_check, (!C.done && C.check) ? 1u : 0u);
     set_cond_if_changed(P, C, CB_SNAP, P.h_snap, (C.n_snap > 0 || C.n_moves > 0) ? 1u : 0u);
     if (P.trace) set_cond_if_changed(P, C, CB_TRACE, P.h_trace, C.hash_pending ? 1u : 0u);
+    // the fused pass while every row kernel runs full width (the narrow
+    // single-block passes keep the separate kernels)
+    if (P.use_pass) set_cond_if_changed(P, C, CB_FUSED, P.h_fused, C.active > P.W / 2 ? 1u : 0u);
   }
   decide_mark(P, plain, 22);
 }
@@ -1673,21 +1746,36 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
 // Folds the finished launches' entry/exit stamps into the accumulators and
 // credits this iteration's row kernels with their algorithmic bytes
 // (compulsory traffic, gathers counted once).
-// Called by the first K_KINDS threads (one kind each).
+// Called by one full warp (lane k folds kind k); the fused pass, when it ran
+// this iteration, is credited with the primal's and the dual's bytes.
 static __device__ void prof_fold(const Params& P, const Ctrl& C, int k, unsigned long long now) {
-  if (!P.prof || k >= K_KINDS) return;
-  const unsigned long long s = P.prof[2 * k], e = P.prof[2 * k + 1];
-  if (e != 0ull && s != ~0ull && e >= s) {
-    P.prof_acc[3 * k] += (double)(e - s);
-    P.prof_acc[3 * k + 1] += 1.0;
+  if (!P.prof) return;
+  unsigned long long s = ~0ull, e = 0ull;
+  if (k < K_KINDS) {
+    s = P.prof[2 * k];
+    e = P.prof[2 * k + 1];
   }
-  P.prof[2 * k] = k == K_DECIDE ? now : ~0ull;
-  P.prof[2 * k + 1] = 0ull;
+  const bool ran = e != 0ull && s != ~0ull && e >= s;
+  const bool ran_pass = __shfl_sync(0xffffffffu, ran ? 1 : 0, K_PASS) != 0;
+  if (k < K_KINDS) {
+    if (ran) {
+      P.prof_acc[3 * k] += (double)(e - s);
+      P.prof_acc[3 * k + 1] += 1.0;
+    }
+    P.prof[2 * k] = k == K_DECIDE ? now : ~0ull;
+    P.prof[2 * k + 1] = 0ull;
+  }
   if (k != 0) return;
   const double n = P.n, m = P.m, nnz = (double)P.nnz, K = C.active;
   const double chk = C.check ? 1.0 : 0.0;
-  P.prof_acc[3 * K_PRIMAL + 2] += 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 4.0 * n + chk * n);
-  P.prof_acc[3 * K_DUAL + 2] += 12.0 * nnz + 4.0 * (m + 1) + 16.0 * m + 8.0 * K * (n + 6.0 * m + chk * 3.0 * m);
+  const double bp = 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 4.0 * n + chk * n);
+  const double bd = 12.0 * nnz + 4.0 * (m + 1) + 16.0 * m + 8.0 * K * (n + 6.0 * m + chk * 3.0 * m);
+  if (ran_pass) {
+    P.prof_acc[3 * K_PASS + 2] += bp + bd;
+  } else {
+    P.prof_acc[3 * K_PRIMAL + 2] += bp;
+    P.prof_acc[3 * K_DUAL + 2] += bd;
+  }
   if (C.check)
     P.prof_acc[3 * K_CHECK + 2] += 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 5.0 * n);
 }
@@ -2648,6 +2736,7 @@ template <int W>
 struct WLaunch {
   static void iteration_check(const Params& P, cudaStream_t s);
   static void iteration_plain(const Params& P, cudaStream_t s);
+  static void pass(const Params& P, cudaStream_t s);
   static void spmm(const Params& P, cudaStream_t s, bool transpose, const double* in,
                    double* out, int active, int R);
   static void cert(const Params& P, cudaStream_t s);
@@ -2692,6 +2781,11 @@ template <int W>
 void WLaunch<W>::iteration_plain(const Params& P, cudaStream_t s) {
   k_primal<W, false><<<grid_of((const void*)k_primal<W, false>), kBlock, 0, s>>>(P);
   k_dual<W, false><<<grid_of((const void*)k_dual<W, false>), kBlock, 0, s>>>(P);
+}
+
+template <int W>
+void WLaunch<W>::pass(const Params& P, cudaStream_t s) {
+  k_pass<W><<<grid_of((const void*)k_pass<W>), kBlock, 0, s>>>(P);
 }
 
 template <int W>
