@@ -473,7 +473,7 @@ def main():
             a[0] += lau
             a[1] += ns
             a[2] += by
-    row = {k: v for k, v in prof.items() if k in ("primal", "dual", "check", "pass") and v[1] > 0}
+    row = {k: v for k, v in prof.items() if k in ("primal", "dual", "check") and v[1] > 0}
     dom = max(row, key=lambda k: row[k][1]) if row else None
     peak, peak_kind = peaks()
     roof = None

@@ -207,10 +207,6 @@ void launch_iteration_plain(const Params& P, cudaStream_t s) {
   BL_DISPATCH_W(P.W, WLaunch<W_>::iteration_plain(P, s));
 }
 
-void launch_pass(const Params& P, cudaStream_t s) {
-  BL_DISPATCH_W(P.W, WLaunch<W_>::pass(P, s));
-}
-
 int loop_ctas_per_sm(int W) {
   int occ = 1;
   BL_DISPATCH_W(W, occ = WLaunch<W_>::loop_ctas_per_sm());

@@ -966,59 +966,6 @@ __global__ void __launch_bounds__(kBlock, kDualMinCtas) k_dual(Params P) {
 }
 
 // ---------------------------------------------------------------------------
-// fused plain pass: per column block, the primal items then the dual items
-// ---------------------------------------------------------------------------
-// One launch walks (block b: Rp primal items, then Rd dual items) in ticket
-// order; a CTA that draws a dual item of block b waits until all of b's
-// primal items are done (their XT rows written, their sums folded). The dual
-// then gathers XT(b) and streams Y(b) while the primal has just written /
-// gathered them, instead of one whole-K pass later when they left L2 (C4:
-// the separate dual reads 1.86x its algorithmic DRAM bytes). Sums, order of
-// operations and results are those of k_primal followed by k_dual.
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <int W>
-__global__ void __launch_bounds__(kBlock, kDualMinCtas) k_pass(Params P) {
-  __shared__ double red[kRedDoubles];
-  __shared__ Ctrl C;
-  if (threadIdx.x == 0) C = *P.ctrl;
-  __syncthreads();
-  if (C.done) return;
-  prof_begin(P, K_PASS);
-  const int nb = (C.active + W - 1) / W;
-  const int Rp = C.Rp, Rd = C.Rd, per = Rp + Rd;
-  int* pdone = P.pdone;
-  auto item = [&](int w) {
-    const int b = w / per, k = w - b * per;
-    if (k < Rp) {
-      PrimalOp<W, false> op(P, C);
-      run_item<W, 2>(op, b, k, P.n, Rp, P.partials, P.counters, P.colsum, S_DX2, P.Kp, red);
-      if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(pdone + b, 1);
-      }
-    } else {
-      if (threadIdx.x == 0) {
-        while (ld_acquire_gpu(pdone + b) < Rp) __nanosleep(128);
-        __threadfence();  // (gpu scope: also drops stale L1 lines before the XT gathers)
-      }
-      __syncthreads();
-      DualOp<W, false> op(P, C);
-      run_item<W, DualOp<W, false>::NS>(op, b, k - Rp, P.m, Rd, P.partials + P.part_stride,
-                                        P.counters + P.cnt_stride, P.colsum, S_DY2, P.Kp, red);
-    }
-  };
-  ticket_items(P.ticket, nb * per, item, [&] {
-    for (int b = 0; b < nb; ++b) pdone[b] = 0;
-  });
-  prof_end(P, K_PASS);
-}
-
-// ---------------------------------------------------------------------------
 // check: AT_YT = A'YT, reduced costs and the column-space check terms
 // ---------------------------------------------------------------------------
 template <int W>
@@ -1736,9 +1683,6 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
     set_cond_if_changed(P, C, CB_CHECK, P.h_check, (!C.done && C.check) ? 1u : 0u);
     set_cond_if_changed(P, C, CB_SNAP, P.h_snap, (C.n_snap > 0 || C.n_moves > 0) ? 1u : 0u);
     if (P.trace) set_cond_if_changed(P, C, CB_TRACE, P.h_trace, C.hash_pending ? 1u : 0u);
-    // the fused pass while every row kernel runs full width (the narrow
-    // single-block passes keep the separate kernels)
-    if (P.use_pass) set_cond_if_changed(P, C, CB_FUSED, P.h_fused, C.active > P.W / 2 ? 1u : 0u);
   }
   decide_mark(P, plain, 22);
 }
@@ -1746,36 +1690,21 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
 // Folds the finished launches' entry/exit stamps into the accumulators and
 // credits this iteration's row kernels with their algorithmic bytes
 // (compulsory traffic, gathers counted once).
-// Called by one full warp (lane k folds kind k); the fused pass, when it ran
-// this iteration, is credited with the primal's and the dual's bytes.
+// Called by the first K_KINDS threads (one kind each).
 static __device__ void prof_fold(const Params& P, const Ctrl& C, int k, unsigned long long now) {
-  if (!P.prof) return;
-  unsigned long long s = ~0ull, e = 0ull;
-  if (k < K_KINDS) {
-    s = P.prof[2 * k];
-    e = P.prof[2 * k + 1];
+  if (!P.prof || k >= K_KINDS) return;
+  const unsigned long long s = P.prof[2 * k], e = P.prof[2 * k + 1];
+  if (e != 0ull && s != ~0ull && e >= s) {
+    P.prof_acc[3 * k] += (double)(e - s);
+    P.prof_acc[3 * k + 1] += 1.0;
   }
-  const bool ran = e != 0ull && s != ~0ull && e >= s;
-  const bool ran_pass = __shfl_sync(0xffffffffu, ran ? 1 : 0, K_PASS) != 0;
-  if (k < K_KINDS) {
-    if (ran) {
-      P.prof_acc[3 * k] += (double)(e - s);
-      P.prof_acc[3 * k + 1] += 1.0;
-    }
-    P.prof[2 * k] = k == K_DECIDE ? now : ~0ull;
-    P.prof[2 * k + 1] = 0ull;
-  }
+  P.prof[2 * k] = k == K_DECIDE ? now : ~0ull;
+  P.prof[2 * k + 1] = 0ull;
   if (k != 0) return;
   const double n = P.n, m = P.m, nnz = (double)P.nnz, K = C.active;
   const double chk = C.check ? 1.0 : 0.0;
-  const double bp = 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 4.0 * n + chk * n);
-  const double bd = 12.0 * nnz + 4.0 * (m + 1) + 16.0 * m + 8.0 * K * (n + 6.0 * m + chk * 3.0 * m);
-  if (ran_pass) {
-    P.prof_acc[3 * K_PASS + 2] += bp + bd;
-  } else {
-    P.prof_acc[3 * K_PRIMAL + 2] += bp;
-    P.prof_acc[3 * K_DUAL + 2] += bd;
-  }
+  P.prof_acc[3 * K_PRIMAL + 2] += 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 4.0 * n + chk * n);
+  P.prof_acc[3 * K_DUAL + 2] += 12.0 * nnz + 4.0 * (m + 1) + 16.0 * m + 8.0 * K * (n + 6.0 * m + chk * 3.0 * m);
   if (C.check)
     P.prof_acc[3 * K_CHECK + 2] += 12.0 * nnz + 4.0 * (n + 1) + 24.0 * n + 8.0 * K * (m + 5.0 * n);
 }
@@ -2736,7 +2665,6 @@ template <int W>
 struct WLaunch {
   static void iteration_check(const Params& P, cudaStream_t s);
   static void iteration_plain(const Params& P, cudaStream_t s);
-  static void pass(const Params& P, cudaStream_t s);
   static void spmm(const Params& P, cudaStream_t s, bool transpose, const double* in,
                    double* out, int active, int R);
   static void cert(const Params& P, cudaStream_t s);
@@ -2781,11 +2709,6 @@ template <int W>
 void WLaunch<W>::iteration_plain(const Params& P, cudaStream_t s) {
   k_primal<W, false><<<grid_of((const void*)k_primal<W, false>), kBlock, 0, s>>>(P);
   k_dual<W, false><<<grid_of((const void*)k_dual<W, false>), kBlock, 0, s>>>(P);
-}
-
-template <int W>
-void WLaunch<W>::pass(const Params& P, cudaStream_t s) {
-  k_pass<W><<<grid_of((const void*)k_pass<W>), kBlock, 0, s>>>(P);
 }
 
 template <int W>

@@ -350,10 +350,7 @@ void build_graph(bl_ctx* ctx, bl::Params P) {
   ht = 0;
   if (P.trace)  // an unused handle makes instantiation fail
     ck(cudaGraphConditionalHandleCreate(&ht, g, 0, cudaGraphCondAssignDefault), "handle");
-  cudaGraphConditionalHandle hf = 0;
-  if (P.use_pass)
-    ck(cudaGraphConditionalHandleCreate(&hf, g, 1, cudaGraphCondAssignDefault), "handle");
-  P.h_fused = hf;
+
   P.use_graph = 1;
   P.h_loop = hl;
   P.h_check = hc;
@@ -366,15 +363,7 @@ void build_graph(bl_ctx* ctx, bl::Params P) {
   cudaGraphNode_t n_it = add_cond(wbody, nullptr, 0, hc, cudaGraphCondTypeIf, 2, ifb);
   cudaStream_t s2 = ctx->side;
   capture_into(s2, ifb[0], [&] { bl::launch_iteration_check(P, s2); });
-  if (P.use_pass) {
-    // plain iterations: IF(fused) { k_pass } ELSE { k_primal; k_dual }
-    cudaGraph_t pb[2];
-    add_cond(ifb[1], nullptr, 0, hf, cudaGraphCondTypeIf, 2, pb);
-    capture_into(s2, pb[0], [&] { bl::launch_pass(P, s2); });
-    capture_into(s2, pb[1], [&] { bl::launch_iteration_plain(P, s2); });
-  } else {
-    capture_into(s2, ifb[1], [&] { bl::launch_iteration_plain(P, s2); });
-  }
+  capture_into(s2, ifb[1], [&] { bl::launch_iteration_plain(P, s2); });
   // decide (phase 0) then the conditional tails, captured into the body
   cudaStream_t s = s2;
   ck(cudaStreamBeginCaptureToGraph(s, wbody, &n_it, nullptr, 1, cudaStreamCaptureModeRelaxed),
@@ -472,7 +461,6 @@ void run_loop_steps(bl_ctx* ctx, bl::Params P) {
     ck(cudaStreamSynchronize(s), "step sync");
     if (h->done) break;
     if (h->check) bl::launch_iteration_check(P, s);
-    else if (P.use_pass && h->active > P.W / 2) bl::launch_pass(P, s);
     else bl::launch_iteration_plain(P, s);
     bl::launch_decide(P, s, 0);
     bl::launch_cert(P, s);
@@ -660,8 +648,7 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
   P.move_src = si + 4 * (size_t)Kp;
   P.snap_orig = si + 5 * (size_t)Kp;
   P.err_flag = si + 6 * (size_t)Kp;
-  P.pdone = P.err_flag + 1;  // nb <= Kp / W < Kp - 1 entries
-  ck(cudaMemsetAsync(P.err_flag, 0, sizeof(int) * (size_t)Kp, s), "err flag / pass counters");
+  ck(cudaMemsetAsync(P.err_flag, 0, sizeof(int), s), "err flag");
   int* oi = static_cast<int*>(ctx->buf[bl_ctx::B_ORIGI].ensure(sizeof(int) * 3 * (size_t)width));
   P.orig_done = oi;
   P.ov_beg = oi + width;
@@ -723,13 +710,10 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
                                                        items_for(n, W, grid)));
   P.partials = static_cast<double*>(
       ctx->buf[bl_ctx::B_PART].ensure(sizeof(double) * max_items * 10 * W));
-  P.part_stride = max_items * 2 * W;  // the fused pass's dual partials (<= 3 sums) follow
   // per-block fold counters, then the row kernels' work-item ticket
-  // two banks (the fused pass's primal and dual items run concurrently)
   const int cbank = std::max(nb, 64);
   P.counters = static_cast<int*>(
-      ctx->buf[bl_ctx::B_CNT].ensure(sizeof(int) * (2 * (size_t)cbank + 2)));
-  P.cnt_stride = cbank;
+      ctx->buf[bl_ctx::B_CNT].ensure(sizeof(int) * ((size_t)cbank + 2)));
   // Block-major dynamic work items pay off once one column block's gathered
   // operand is a sizeable share of L2 (C4: -21% per row pass, measured); on
   // small problems the per-item atomics cost more than the drift they
@@ -740,10 +724,8 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
       return e ? std::atof(e) : 4.0 * (1 << 20);
     }();
     const double block_operand = 8.0 * W * (double)std::max(m, n);
-    P.ticket = block_operand >= min_bytes ? P.counters + 2 * cbank : nullptr;
+    P.ticket = block_operand >= min_bytes ? P.counters + cbank : nullptr;
   }
-  // the fused per-block pass needs the ticket's block-major order
-  P.use_pass = (P.ticket != nullptr && !std::getenv("BATCHLP_NO_PASS")) ? 1 : 0;
   P.snap_list = static_cast<int*>(ctx->buf[bl_ctx::B_SNAP].ensure(sizeof(int) * 3 * (size_t)Kp));
   P.moves = static_cast<int*>(ctx->buf[bl_ctx::B_MOVES].ensure(sizeof(int) * 2 * (size_t)Kp));
   P.log_cap = 1 << 16;
@@ -844,7 +826,7 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
       hoi[2 * (size_t)width + j] = oe[j];
     }
     ck(cudaMemcpyAsync(oi, hoi.data(), sizeof(int) * hoi.size(), cudaMemcpyHostToDevice, s), "origi");
-    ck(cudaMemsetAsync(P.counters, 0, sizeof(int) * (2 * (size_t)std::max(nb, 64) + 2), s), "counters");
+    ck(cudaMemsetAsync(P.counters, 0, sizeof(int) * ((size_t)std::max(nb, 64) + 2), s), "counters");
     ck(cudaMemsetAsync(P.res, 0, sizeof(bl_column_result) * (size_t)width, s), "res");
     ck(cudaMemsetAsync(P.colsum, 0, sizeof(double) * bl::S_COUNT * (size_t)Kp, s), "colsum");
   }
@@ -975,7 +957,7 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
     static const char* names[bl::K_KINDS] = {"primal",      "dual",      "check",
                                              "decide",      "cert",      "snapshot",
                                              "compact",     "trace",     "tail_primal",
-                                             "tail_dual",   "tail_decide", "pass"};
+                                             "tail_dual",   "tail_decide"};
     ctx->last_prof.assign(bl::K_KINDS, bl_kernel_stat{});
     for (int k = 0; k < bl::K_KINDS; ++k) {
       bl_kernel_stat& st = ctx->last_prof[k];

@@ -55,7 +55,7 @@ def main():
             ms.append(summ.device_ms)
         dev_ms = min(ms)
         prof = summ.profile
-        rk = {k: v for k, v in prof.items() if k in ("primal", "dual", "pass") and v[1] > 0}
+        rk = {k: v for k, v in prof.items() if k in ("primal", "dual") and v[1] > 0}
         dom = max(rk, key=lambda k: rk[k][1]) if rk else None
         kern = None
         if dom:
