@@ -498,6 +498,7 @@ __device__ __forceinline__ void run_item(Op& op, int b, int r, int rows, int R,
 #ifndef BL_DYNAMIC_ITEMS
 #define BL_DYNAMIC_ITEMS 1
 #endif
+
 // Items [0, items) handed to the grid from one atomic ticket, in order (the
 // next one fetched while the current item runs), so every CTA works on the
 // column block the grid is on: only ~one block's gathered operand is live in
