@@ -207,6 +207,14 @@ void launch_iteration_plain(const Params& P, cudaStream_t s) {
   BL_DISPATCH_W(P.W, WLaunch<W_>::iteration_plain(P, s));
 }
 
+void launch_iteration_check_narrow(const Params& P, cudaStream_t s) {
+  BL_DISPATCH_W(P.W, WLaunch<W_>::iteration_check_narrow(P, s));
+}
+
+void launch_iteration_plain_narrow(const Params& P, cudaStream_t s) {
+  BL_DISPATCH_W(P.W, WLaunch<W_>::iteration_plain_narrow(P, s));
+}
+
 int loop_ctas_per_sm(int W) {
   int occ = 1;
   BL_DISPATCH_W(W, occ = WLaunch<W_>::loop_ctas_per_sm());

@@ -313,6 +313,29 @@ __device__ __forceinline__ double m_residual(double dx2, double dy2, double cros
   return sqrt(msq);
 }
 
+// Warp 0 of the CTA that folded a column block's dual sums: the block's
+// M-norm residuals (m_residual_from_terms, solver.hpp:250-263) and their
+// sequential sum. Out of line, so the dual's row loop is register-allocated
+// without it.
+static __device__ __noinline__ void fold_residuals(const double* colsum, int Kp,
+                                                   const double* w, double eta, int j0,
+                                                   int valid, double* resid, double* blk,
+                                                   int* err_flag) {
+  const int lane = threadIdx.x;
+  const int j = j0 + lane;
+  double r = 0.0;
+  if (lane < valid) {
+    int err = 0;
+    r = m_residual(colsum[(size_t)S_DX2 * Kp + j], colsum[(size_t)S_DY2 * Kp + j],
+                   colsum[(size_t)S_CROSS * Kp + j], eta, w[j], &err);
+    resid[j] = r;
+    if (err) atomicOr(err_flag, 1);
+  }
+  double sum = 0.0;
+  for (int k = 0; k < valid; ++k) sum += __shfl_sync(0xffffffffu, r, k);
+  if (lane == 0) *blk = sum;
+}
+
 // ---------------------------------------------------------------------------
 // deterministic per-column reduction of one work item
 // ---------------------------------------------------------------------------
@@ -776,24 +799,31 @@ static __device__ void primal_body(const Params& P, const Ctrl& C, double* red) 
   prof_end(P, K_PRIMAL);
 }
 
-// BL_NARROW_ROWS: with one column block left the graph's row kernels walk
-// rows with the narrow lane mapping (only the live slots are gathered).
-#ifndef BL_NARROW_ROWS
-#define BL_NARROW_ROWS 1
-#endif
+// Full-width passes and narrow single-block passes are separate kernels (the
+// graph picks one per pass through IF(narrow), set by the decide): the
+// full-width row loop is register-allocated alone, which keeps it free of
+// spills. Narrow: with one column block left and a LPs live, rows are walked
+// by the smallest power of two of lanes covering them (only live slots are
+// gathered).
 template <int W, bool CHECK>
 __global__ void __launch_bounds__(kBlock, kPrimalMinCtas) k_primal(Params P) {
   __shared__ double red[kRedDoubles];
-  __shared__ Ctrl C;  // shared: the staged row ops re-read it per row
+  __shared__ Ctrl C;
   if (threadIdx.x == 0) C = *P.ctrl;
   __syncthreads();
   if (C.done) return;
-  if constexpr (BL_NARROW_ROWS && W >= 16) {
-    const int Lsel = pass_lanes<W>(C.active);
-    BL_DISPATCH_L(W, Lsel, (primal_body<W, CHECK, LL_>(P, C, red)));
-  } else {
-    primal_body<W, CHECK>(P, C, red);
-  }
+  primal_body<W, CHECK>(P, C, red);
+}
+
+template <int W, bool CHECK>
+__global__ void __launch_bounds__(kBlock, kPrimalMinCtas) k_primal_narrow(Params P) {
+  __shared__ double red[kRedDoubles];
+  __shared__ Ctrl C;
+  if (threadIdx.x == 0) C = *P.ctrl;
+  __syncthreads();
+  if (C.done) return;
+  const int Lsel = pass_lanes<W>(C.active);
+  BL_DISPATCH_L(W, Lsel, (primal_body<W, CHECK, LL_>(P, C, red)));
 }
 
 // ---------------------------------------------------------------------------
@@ -844,19 +874,9 @@ struct DualOp {
   // so the single-CTA decide only combines block sums (batch_solver.hpp:
   // 209-222). Warp 0 does it: W <= 32 slots.
   __device__ void after_fold(int b) {
-    if (threadIdx.x >= 32) return;
-    const int lane = threadIdx.x, j = b * W + lane;
-    double r = 0.0;
-    if (lane < W && j < active) {
-      int err = 0;
-      r = m_residual(cs(P, S_DX2, j), cs(P, S_DY2, j), cs(P, S_CROSS, j), P.eta, P.w[j], &err);
-      P.resid[j] = r;
-      if (err) atomicOr(P.err_flag, 1);
-    }
-    double sum = 0.0;
-#pragma unroll
-    for (int k = 0; k < W; ++k) sum += __shfl_sync(0xffffffffu, r, k);
-    if (lane == 0) P.blk_resid[b] = sum;
+    if (threadIdx.x < 32)
+      fold_residuals(P.colsum, P.Kp, P.w, P.eta, b * W, min(W, active - b * W), P.resid,
+                     P.blk_resid + b, P.err_flag);
   }
   __device__ void row(int b, int i, int, int li, double (&acc)[NS][V]) {
     const int n = P.n, m = P.m;
@@ -954,16 +974,22 @@ static __device__ void dual_body(const Params& P, const Ctrl& C, double* red) {
 template <int W, bool CHECK>
 __global__ void __launch_bounds__(kBlock, kDualMinCtas) k_dual(Params P) {
   __shared__ double red[kRedDoubles];
-  __shared__ Ctrl C;  // shared: the staged row ops re-read it per row
+  __shared__ Ctrl C;
   if (threadIdx.x == 0) C = *P.ctrl;
   __syncthreads();
   if (C.done) return;
-  if constexpr (BL_NARROW_ROWS && W >= 16) {
-    const int Lsel = pass_lanes<W>(C.active);
-    BL_DISPATCH_L(W, Lsel, (dual_body<W, CHECK, LL_>(P, C, red)));
-  } else {
-    dual_body<W, CHECK>(P, C, red);
-  }
+  dual_body<W, CHECK>(P, C, red);
+}
+
+template <int W, bool CHECK>
+__global__ void __launch_bounds__(kBlock, kPrimalMinCtas) k_dual_narrow(Params P) {
+  __shared__ double red[kRedDoubles];
+  __shared__ Ctrl C;
+  if (threadIdx.x == 0) C = *P.ctrl;
+  __syncthreads();
+  if (C.done) return;
+  const int Lsel = pass_lanes<W>(C.active);
+  BL_DISPATCH_L(W, Lsel, (dual_body<W, CHECK, LL_>(P, C, red)));
 }
 
 // ---------------------------------------------------------------------------
@@ -1059,12 +1085,16 @@ __global__ void __launch_bounds__(kBlock, kRowMinCtas) k_check(Params P) {
   __shared__ double red[kRedDoubles];
   const Ctrl C = *P.ctrl;
   if (C.done || !C.check) return;
-  if constexpr (BL_NARROW_ROWS && W >= 16) {
-    const int Lsel = pass_lanes<W>(C.active);
-    BL_DISPATCH_L(W, Lsel, (check_body<W, LL_>(P, C, red)));
-  } else {
-    check_body<W>(P, C, red);
-  }
+  check_body<W>(P, C, red);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBlock, kRowMinCtas) k_check_narrow(Params P) {
+  __shared__ double red[kRedDoubles];
+  const Ctrl C = *P.ctrl;
+  if (C.done || !C.check) return;
+  const int Lsel = pass_lanes<W>(C.active);
+  BL_DISPATCH_L(W, Lsel, (check_body<W, LL_>(P, C, red)));
 }
 
 // ---------------------------------------------------------------------------
@@ -1684,6 +1714,12 @@ static __device__ void finalize(const Params& P, Ctrl& C, double mean, double* s
     set_cond_if_changed(P, C, CB_CHECK, P.h_check, (!C.done && C.check) ? 1u : 0u);
     set_cond_if_changed(P, C, CB_SNAP, P.h_snap, (C.n_snap > 0 || C.n_moves > 0) ? 1u : 0u);
     if (P.trace) set_cond_if_changed(P, C, CB_TRACE, P.h_trace, C.hash_pending ? 1u : 0u);
+    // narrow row kernels once a single block with <= W/2 live LPs is left
+    if (P.narrow_ok) {
+      const unsigned nw = C.active <= P.W / 2 ? 1u : 0u;
+      if (((C.cond >> CB_NARROW) & 1) != (int)nw) set_cond(P, P.h_narrow2, nw);
+      set_cond_if_changed(P, C, CB_NARROW, P.h_narrow, nw);
+    }
   }
   decide_mark(P, plain, 22);
 }
@@ -2666,6 +2702,8 @@ template <int W>
 struct WLaunch {
   static void iteration_check(const Params& P, cudaStream_t s);
   static void iteration_plain(const Params& P, cudaStream_t s);
+  static void iteration_check_narrow(const Params& P, cudaStream_t s);
+  static void iteration_plain_narrow(const Params& P, cudaStream_t s);
   static void spmm(const Params& P, cudaStream_t s, bool transpose, const double* in,
                    double* out, int active, int R);
   static void cert(const Params& P, cudaStream_t s);
@@ -2710,6 +2748,19 @@ template <int W>
 void WLaunch<W>::iteration_plain(const Params& P, cudaStream_t s) {
   k_primal<W, false><<<grid_of((const void*)k_primal<W, false>), kBlock, 0, s>>>(P);
   k_dual<W, false><<<grid_of((const void*)k_dual<W, false>), kBlock, 0, s>>>(P);
+}
+
+template <int W>
+void WLaunch<W>::iteration_check_narrow(const Params& P, cudaStream_t s) {
+  k_primal_narrow<W, true><<<grid_of((const void*)k_primal_narrow<W, true>), kBlock, 0, s>>>(P);
+  k_dual_narrow<W, true><<<grid_of((const void*)k_dual_narrow<W, true>), kBlock, 0, s>>>(P);
+  k_check_narrow<W><<<grid_of((const void*)k_check_narrow<W>), kBlock, 0, s>>>(P);
+}
+
+template <int W>
+void WLaunch<W>::iteration_plain_narrow(const Params& P, cudaStream_t s) {
+  k_primal_narrow<W, false><<<grid_of((const void*)k_primal_narrow<W, false>), kBlock, 0, s>>>(P);
+  k_dual_narrow<W, false><<<grid_of((const void*)k_dual_narrow<W, false>), kBlock, 0, s>>>(P);
 }
 
 template <int W>

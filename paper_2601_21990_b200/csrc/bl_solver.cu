@@ -350,6 +350,14 @@ void build_graph(bl_ctx* ctx, bl::Params P) {
   ht = 0;
   if (P.trace)  // an unused handle makes instantiation fail
     ck(cudaGraphConditionalHandleCreate(&ht, g, 0, cudaGraphCondAssignDefault), "handle");
+  // one handle per conditional node: the check and the plain branch each get one
+  cudaGraphConditionalHandle hn = 0, hn2 = 0;
+  if (P.narrow_ok) {
+    ck(cudaGraphConditionalHandleCreate(&hn, g, 0, cudaGraphCondAssignDefault), "handle");
+    ck(cudaGraphConditionalHandleCreate(&hn2, g, 0, cudaGraphCondAssignDefault), "handle");
+  }
+  P.h_narrow = hn;
+  P.h_narrow2 = hn2;
 
   P.use_graph = 1;
   P.h_loop = hl;
@@ -362,8 +370,19 @@ void build_graph(bl_ctx* ctx, bl::Params P) {
   cudaGraph_t ifb[2];
   cudaGraphNode_t n_it = add_cond(wbody, nullptr, 0, hc, cudaGraphCondTypeIf, 2, ifb);
   cudaStream_t s2 = ctx->side;
-  capture_into(s2, ifb[0], [&] { bl::launch_iteration_check(P, s2); });
-  capture_into(s2, ifb[1], [&] { bl::launch_iteration_plain(P, s2); });
+  if (P.narrow_ok) {
+    // each branch: IF(narrow) { single-block narrow kernels } ELSE { full width }
+    cudaGraph_t cb[2], pb[2];
+    add_cond(ifb[0], nullptr, 0, hn, cudaGraphCondTypeIf, 2, cb);
+    add_cond(ifb[1], nullptr, 0, hn2, cudaGraphCondTypeIf, 2, pb);
+    capture_into(s2, cb[0], [&] { bl::launch_iteration_check_narrow(P, s2); });
+    capture_into(s2, cb[1], [&] { bl::launch_iteration_check(P, s2); });
+    capture_into(s2, pb[0], [&] { bl::launch_iteration_plain_narrow(P, s2); });
+    capture_into(s2, pb[1], [&] { bl::launch_iteration_plain(P, s2); });
+  } else {
+    capture_into(s2, ifb[0], [&] { bl::launch_iteration_check(P, s2); });
+    capture_into(s2, ifb[1], [&] { bl::launch_iteration_plain(P, s2); });
+  }
   // decide (phase 0) then the conditional tails, captured into the body
   cudaStream_t s = s2;
   ck(cudaStreamBeginCaptureToGraph(s, wbody, &n_it, nullptr, 1, cudaStreamCaptureModeRelaxed),
@@ -460,8 +479,14 @@ void run_loop_steps(bl_ctx* ctx, bl::Params P) {
     ck(cudaMemcpyAsync(h, P.ctrl, sizeof(bl::Ctrl), cudaMemcpyDeviceToHost, s), "ctrl");
     ck(cudaStreamSynchronize(s), "step sync");
     if (h->done) break;
-    if (h->check) bl::launch_iteration_check(P, s);
-    else bl::launch_iteration_plain(P, s);
+    const bool narrow = P.narrow_ok && h->active <= P.W / 2;
+    if (h->check) {
+      if (narrow) bl::launch_iteration_check_narrow(P, s);
+      else bl::launch_iteration_check(P, s);
+    } else {
+      if (narrow) bl::launch_iteration_plain_narrow(P, s);
+      else bl::launch_iteration_plain(P, s);
+    }
     bl::launch_decide(P, s, 0);
     bl::launch_cert(P, s);
     bl::launch_decide(P, s, 1);
@@ -726,6 +751,11 @@ void solve_batch_impl(bl_ctx* ctx, bl_problem* p, int32_t width, int32_t mode,
     const double block_operand = 8.0 * W * (double)std::max(m, n);
     P.ticket = block_operand >= min_bytes ? P.counters + cbank : nullptr;
   }
+  // narrow single-block row kernels in the graph / step drivers: only large
+  // problems reach a single block there (small ones hand over to the
+  // persistent / cluster kernels first), so only they carry the IF(narrow)
+  // branches (two extra conditional nodes per pass)
+  P.narrow_ok = (W >= 16 && P.ticket != nullptr) ? 1 : 0;
   P.snap_list = static_cast<int*>(ctx->buf[bl_ctx::B_SNAP].ensure(sizeof(int) * 3 * (size_t)Kp));
   P.moves = static_cast<int*>(ctx->buf[bl_ctx::B_MOVES].ensure(sizeof(int) * 2 * (size_t)Kp));
   P.log_cap = 1 << 16;
