@@ -270,19 +270,20 @@ __device__ __forceinline__ void gather_row_grp(const int* __restrict__ rp,
       myv = __ldg(cv + k);
     }
     const int cnt = min(L, e - ch);
-    for (int t = 0; t < cnt; t += 4) {
-      int c[4];
-      double a[4], x[4][V];
+    constexpr int D = 4;  // gathers in flight per batch
+    for (int t = 0; t < cnt; t += D) {
+      int c[D];
+      double a[D], x[D][V];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < D; ++q) {
         c[q] = __shfl_sync(mask, myc, t + q, L);
         a[q] = __shfl_sync(mask, myv, t + q, L);
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < D; ++q)
         if (t + q < cnt) ld_gather<V>(base + (size_t)c[q] * W, x[q]);
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < D; ++q)
         if (t + q < cnt) {
 #pragma unroll
           for (int v = 0; v < V; ++v) acc[v] = __dadd_rn(acc[v], __dmul_rn(a[q], x[q][v]));
