@@ -438,11 +438,26 @@ __device__ __forceinline__ void publish_item(double (&acc)[NS][Geo<W>::V], int b
 }
 
 // Column descriptor of one LP slot as staged in shared memory (ColInfo).
+// 11 words, doubles as (lo, hi) word pairs: a lane reads its slots at a
+// stride of 22 words, so the 16 lanes of a row group hit 16 distinct banks
+// (a 48-byte record put lanes 0, 4, 8, 12 on one bank: 4-way conflicts on
+// every per-row descriptor read).
 struct SColInfo {
   int valid, orig, ob, oe, v0, k0;
-  double val0, step;
-  int fast, pad;  // fast: single-point column (see ColInfo)
+  int fast;  // single-point column (see ColInfo)
+  int val0_w[2], step_w[2];
 };
+static_assert(sizeof(SColInfo) == 44, "SColInfo: odd word stride");
+__device__ __forceinline__ double scol_step(const volatile SColInfo* s) {
+  return __hiloint2double(s->step_w[1], s->step_w[0]);
+}
+__device__ __forceinline__ double scol_val0(const volatile SColInfo* s) {
+  return __hiloint2double(s->val0_w[1], s->val0_w[0]);
+}
+__device__ __forceinline__ void scol_set_step(volatile SColInfo* s, double v) {
+  s->step_w[0] = __double2loint(v);
+  s->step_w[1] = __double2hiint(v);
+}
 
 // One shared array of column descriptors per CTA, whichever run_rows
 // instantiation uses it (a __shared__ in a non-template function has a
@@ -680,8 +695,8 @@ __device__ __forceinline__ ColInfo read_col(const volatile SColInfo* s) {
   c.oe = s->oe;
   c.v0 = s->v0;
   c.k0 = s->k0;
-  c.val0 = s->val0;
-  c.step = s->step;
+  c.val0 = scol_val0(s);
+  c.step = scol_step(s);
   c.fast = s->fast;
   return c;
 }
@@ -695,8 +710,9 @@ __device__ __forceinline__ void stage_col(const Params& P, int j, int active, bo
   s->oe = c.oe;
   s->v0 = c.v0;
   s->k0 = c.k0;
-  s->val0 = c.val0;
-  s->step = c.step;
+  s->val0_w[0] = __double2loint(c.val0);
+  s->val0_w[1] = __double2hiint(c.val0);
+  scol_set_step(s, c.step);
   s->fast = c.fast;
 }
 
@@ -749,12 +765,12 @@ struct PrimalOp {
       const volatile SColInfo* sc = col + v;
       double cc = bc, lo = bl, hi = bh;
       if (sc->fast) {
-        if (sc->v0 == i) apply_ov(sc->k0, sc->val0, cc, lo, hi);
+        if (sc->v0 == i) apply_ov(sc->k0, scol_val0(sc), cc, lo, hi);
       } else {
         col_vals(P, read_col(sc), i, bc, bl, bh, cc, lo, hi);
       }
       const double t = cc + aty[v];
-      xt[v] = project_box(x[v] - sc->step * t, lo, hi);
+      xt[v] = project_box(x[v] - scol_step(sc) * t, lo, hi);
       const double dx = xt[v] - x[v];
       const double da = x[v] - ax[v];
       if (sc->valid) {
@@ -917,7 +933,7 @@ struct DualOp {
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const volatile SColInfo* sc = col + v;
-      const double sigma = sc->step;
+      const double sigma = scol_step(sc);
       const int valid = sc->valid;
       // dual_step_element, solver.hpp:186-190
       const double vv = 2.0 * axt[v] - ax[v];
@@ -2417,8 +2433,8 @@ static __device__ void tail_decide(const Params& P) {
       if (blockIdx.x == 0) P.w[lane] = nw;
       // StepParams (solver.hpp:58-59), as load_col computes them
       tail_w()[lane] = nw;
-      tail_cols(0)[lane].step = P.eta / nw;
-      tail_cols(1)[lane].step = P.eta * nw;
+      scol_set_step(tail_cols(0) + lane, P.eta / nw);
+      scol_set_step(tail_cols(1) + lane, P.eta * nw);
     }
   }
   __syncwarp();  // every lane has read the control block
